@@ -1,0 +1,423 @@
+"""Benchmark of the B200 FP64 7-point Jacobi hot path (BASELINE.json metric).
+
+Workload (N=1): BASELINE.json configs[1] — 512^3 interior in 514^3 storage,
+two grids (2.2 GB), interior U[0,1) seeded (seed 42), Dirichlet ring 0.0,
+100 sweeps.  One "step" = the full 100-sweep solve.  For N>1 (torchrun, one
+process per GPU) the same 512^3 block is owned by every rank as a z-slab of a
+512 x 512 x 512N global grid with t-deep ghost planes exchanged over NCCL once
+per fused pass (weak scaling).
+
+Metric: GLUP/s = interior cells x sweeps / time (the reference's LUP
+accounting, sp/pipeline.py:545).  Inputs (2.2 GB) are larger than L2 (126 MB),
+so no explicit flush is needed between steps.
+
+--impl reference: the reference CPU path (the oracle's C port of
+reference_sweep, all host threads) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "GLUP/s FP64 3D 7-pt Jacobi at 1/2/4/8 B200; % of HBM roofline (B/LUP)"
+UNIT = "GLUP/s"
+N_INT = 512
+SWEEPS = 100
+SEED = 42
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            for k, name in enumerate(names):
+                if r[5 + k].lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / cpu baseline: the oracle's C port of reference_sweep
+# ---------------------------------------------------------------------------
+
+def cpu_rate(target_s: float = 12.0, max_sweeps: int = 100):
+    """Time the reference CPU path (oracle C port of sp/kernel.py:99-111, all
+    host threads) on the C2 grid for ~target_s seconds.  Returns
+    (GLUP/s, threads, sample description)."""
+    import numpy as np  # noqa: F401
+    import oracle
+    n = (N_INT, N_INT, N_INT)
+    d = oracle.make_storage(*n, init="random", seed=SEED)
+    a, b = d, d.copy()
+    L = oracle.lib()
+    threads = L.or_max_threads()
+    done = 0
+    t0 = time.perf_counter()
+    while done < max_sweeps:
+        oracle.c_sweeps(a, b, n, 1, threads=threads)
+        a, b = b, a
+        done += 1
+        if time.perf_counter() - t0 >= target_s:
+            break
+    dt = time.perf_counter() - t0
+    rate = N_INT ** 3 * done / dt / 1e9
+    sample = (f"{done} reference sweeps of the 512^3 C2 grid (oracle C port of reference_sweep, "
+              f"OpenMP over z, {threads} threads) in {dt:.1f} s")
+    return rate, threads, sample
+
+
+def run_reference_arm(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    n = (N_INT, N_INT, N_INT)
+    d = oracle.make_storage(*n, init="random", seed=SEED)
+    a, b = d, d.copy()
+    threads = oracle.lib().or_max_threads()
+    # each step: a bounded sample of the workload (SPS sweeps of the C2 grid)
+    sps = args.ref_sweeps_per_step
+    for _ in range(args.warmup):
+        oracle.c_sweeps(a, b, n, sps, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.c_sweeps(a, b, n, sps, threads=threads)
+    dt = time.perf_counter() - t0
+    value = N_INT ** 3 * sps * args.steps / dt / 1e9
+    sample = (f"{sps} reference sweeps of the 512^3 C2 grid per step (oracle C port of "
+              f"reference_sweep, sp/kernel.py:99-111; OpenMP, {threads} threads)")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64, seed 42)",
+        "config": {"workload": "C2: 512^3 FP64 7-pt Jacobi, two grids, ring 0.0",
+                   "sweeps_per_step": sps, "l2_flush": "inputs 2.2 GB > L2"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def plan_depths(total: int, t: int):
+    """Fused-pass depths summing to `total` with passes of at most t."""
+    n = -(-total // t)
+    base, extra = divmod(total, n)
+    return [base + (1 if k < extra else 0) for k in range(n)]
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1006_3148_b200 as sp
+    from paper_1006_3148_b200 import _lib
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    L = _lib.load()
+    peak, peak_src = _peaks()
+
+    def barrier_sync():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # --- the solve object for this rank ---------------------------------------
+    if ws > 1:
+        from paper_1006_3148_b200 import halo
+        solver = halo.SlabSolver.weak(per_rank=(N_INT, N_INT, N_INT), seed=SEED, ring=0.0,
+                                      depth=args.t)
+        lups_rank = N_INT ** 3 * SWEEPS
+
+        def step(timer=None):
+            solver.run_sweeps(SWEEPS, timer=timer)
+
+        grid_bytes = solver.storage_bytes()
+    else:
+        g0 = sp.create_grid(N_INT, N_INT, N_INT, init="random", seed=SEED)
+        a, b = g0, g0.copy()
+        lups_rank = N_INT ** 3 * SWEEPS
+        grid_bytes = a.data.numel() * 8
+        depths = plan_depths(SWEEPS, args.t)
+        bufs = [a, b]
+
+        def step(timer=None):
+            cur = 0
+            for c in depths:
+                if timer is not None:
+                    timer.start(c)
+                sp.fused_sweeps(bufs[cur], bufs[1 - cur], c)
+                if timer is not None:
+                    timer.stop()
+                cur = 1 - cur
+
+    class LaunchTimer:
+        """CUDA events around every fused launch on the launching stream."""
+
+        def __init__(self):
+            self.ev = []
+
+        def start(self, depth):
+            s = torch.cuda.Event(enable_timing=True)
+            s.record()
+            self.ev.append([depth, s, None])
+
+        def stop(self):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.ev[-1][2] = e
+
+        def stats(self):
+            ms = [s.elapsed_time(e) for _, s, e in self.ev]
+            return ms, [d for d, _, _ in self.ev]
+
+    # --- warmup + timed region ------------------------------------------------
+    for _ in range(args.warmup):
+        step()
+    clocks = Clocks(local)
+    barrier_sync()
+    clocks.start()
+    L.sp_launch_count(1)
+    timer = LaunchTimer()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    barrier_sync()
+    ev0.record()
+    for _ in range(args.steps):
+        step(timer)
+    ev1.record()
+    barrier_sync()
+    launches = int(L.sp_launch_count(0))
+    clk = clocks.stop()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    if ws > 1:
+        t = torch.tensor([elapsed_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    value = lups_rank * ws * args.steps / (elapsed_ms / 1e3) / 1e9
+    ms, ds = timer.stats()
+    dom_depth = max(set(ds), key=ds.count) if ds else args.t
+    dom = [m for m, d in zip(ms, ds) if d == dom_depth]
+    avg_ms = sum(dom) / len(dom) if dom else elapsed_ms / args.steps
+    # algorithmic bytes per fused launch: one read + one write of every
+    # interior cell (16 B/LUP / depth x depth levels)
+    alg_bytes = 16.0 * N_INT ** 3
+    achieved = alg_bytes / (avg_ms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                pt = json.load(f)
+            traffic = pt.get(f"k_temporal_T{dom_depth}", {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    extra = {}
+    if rank == 0 and ws == 1 and not args.quick:
+        # per-depth GLUP/s (t=1 is the plain sweep K1), 3 timed solves each
+        per = {}
+        for t in (1, 2, 3, 4):
+            d_t = plan_depths(SWEEPS, t)
+            cur = 0
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            for rep in range(2):
+                for c in d_t:
+                    sp.fused_sweeps(bufs[cur], bufs[1 - cur], c)
+                    cur = 1 - cur
+            torch.cuda.synchronize()
+            e0.record()
+            for rep in range(3):
+                for c in d_t:
+                    sp.fused_sweeps(bufs[cur], bufs[1 - cur], c)
+                    cur = 1 - cur
+            e1.record()
+            torch.cuda.synchronize()
+            ms_t = e0.elapsed_time(e1) / 3
+            glups = N_INT ** 3 * SWEEPS / (ms_t / 1e3) / 1e9
+            per[str(t)] = {"glups": glups, "ms_per_solve": ms_t,
+                           "hbm_roofline_glups": peak / (16.0 / t),
+                           "frac_of_hbm_roofline": glups * (16.0 / t) / peak}
+        extra["per_depth"] = per
+        extra["plain_sweep_glups"] = per["1"]["glups"]
+
+    # --- e2e through the public API with host buffers --------------------------
+    e2e = None
+    if ws == 1 and not args.quick:
+        import numpy as np
+        host_in = torch.empty(tuple(a.data.shape), dtype=torch.float64).pin_memory()
+        host_in.copy_(g0.data.cpu())
+        host_out = torch.empty_like(host_in).pin_memory()
+        cfg = sp.PipelineConfig(spec=sp.BlockSpec(N_INT, 32, 32), t=args.t)
+        passes = SWEEPS // cfg.h
+        ga = sp.Grid3(N_INT, N_INT, N_INT, 0)
+        gb = sp.Grid3(N_INT, N_INT, N_INT, 0)
+
+        def e2e_step():
+            ga.data.copy_(host_in, non_blocking=True)
+            gb.data.copy_(ga.data)  # the partner grid needs the same ring (device copy)
+            st = sp.run_pipelined((ga, gb), cfg, passes)
+            host_out.copy_(st.result.data, non_blocking=True)
+            return st
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        nst = max(2, min(args.steps, 10))
+        e0.record()
+        for _ in range(nst):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        ms_e2e = e0.elapsed_time(e1) / nst
+        e2e = {"value": N_INT ** 3 * cfg.h * passes / (ms_e2e / 1e3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": grid_bytes, "d2h_bytes_per_step": grid_bytes,
+               "ms_per_step": ms_e2e, "sweeps": cfg.h * passes,
+               "api": "Grid3.data.copy_(pinned) -> run_pipelined -> result.data -> pinned"}
+        assert np.isfinite(e2e["value"])
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        r, thr, sample = cpu_rate(args.cpu_seconds)
+        cpu = {"value": r, "unit": UNIT, "cores": thr, "kind": "port", "sample": sample}
+
+    if ws > 1:
+        dist.barrier()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded SplitMix64 U[0,1), seed 42; ring 0.0)",
+            "config": {"workload": ("C2: 512^3 FP64 7-pt Jacobi, two grids (2.2 GB), 100 sweeps"
+                                    if ws == 1 else
+                                    f"C2-per-rank weak scaling: 512x512x{512 * ws} z-slabs, "
+                                    f"{args.t}-deep ghosts via NCCL, 100 sweeps"),
+                       "fused_depth": args.t, "sweeps_per_step": SWEEPS,
+                       "parallelism": f"z-slab x{ws}" if ws > 1 else "single GPU",
+                       "l2_flush": "not needed: 2.2 GB working set > 126 MB L2"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": f"k_temporal<T={dom_depth}>",
+                         "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_ms,
+                         "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        line.update(extra)
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--t", type=int, default=4, help="fused sweeps per HBM pass (1..4)")
+    ap.add_argument("--quick", action="store_true", help="skip per-depth and e2e legs")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-sweeps-per-step", type=int, default=2)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,96 @@
+"""ctypes binding of libsp200.so (include/sp200.h).
+
+The library is built in-tree (``python -m paper_1006_3148_b200._build`` or
+``__graft_entry__.build()``).  There is no CPU fallback: importing the compute
+entry points without the library or without a CUDA device raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsp200.so")
+
+SP_OK = 0
+SP_EINVAL = -1
+SP_EUNSUP = -2
+SP_ECUDA = -3
+SP_ERANGE = -4
+SP_MAX_FUSED = 4
+
+# every symbol include/sp200.h declares (checked by tests/test_capi.py)
+EXPORTS = (
+    "sp_version", "sp_last_error", "sp_launch_count", "sp_fill_seeded",
+    "sp_fill_constant", "sp_sweep", "sp_apply_window", "sp_window_gather",
+    "sp_copy_ring", "sp_write_faces", "sp_temporal", "sp_compressed_workspace",
+    "sp_compressed", "sp_set_tuning", "sp_tma_eligible",
+)
+
+_lib = None
+
+
+class Sp200Error(RuntimeError):
+    """A CUDA-side failure reported by libsp200 (SP_ECUDA / SP_EUNSUP)."""
+
+
+def _declare(L):
+    i64, i32, dp, vp = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p
+    u64, f64 = ctypes.c_uint64, ctypes.c_double
+    sig = {
+        "sp_version": ([], i32),
+        "sp_last_error": ([], ctypes.c_char_p),
+        "sp_launch_count": ([i32], i64),
+        "sp_fill_seeded": ([dp, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64,
+                            u64, f64, f64, f64, vp], i32),
+        "sp_fill_constant": ([dp, i64, f64, vp], i32),
+        "sp_sweep": ([dp, dp, i64, i64, i64, i64, i64, i64, i64, i32, vp], i32),
+        "sp_apply_window": ([dp, dp, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64, dp, vp],
+                            i32),
+        "sp_window_gather": ([dp, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64, dp, vp], i32),
+        "sp_copy_ring": ([dp, dp, i64, i64, i64, i64, i64, i64, i64, vp], i32),
+        "sp_write_faces": ([dp, i64, i64, i64, i64, i64, i64, i64, ctypes.POINTER(dp), i32, vp], i32),
+        "sp_temporal": ([dp, dp, i64, i64, i64, i64, i64, i64, i64, i32, i64, i64, vp], i32),
+        "sp_compressed_workspace": ([i64, i64, i64, i32], i64),
+        "sp_compressed": ([dp, i64, i64, i64, i64, i64, i64, i64, i32, i32, i64, i64, vp,
+                           ctypes.POINTER(dp), i32, vp], i32),
+        "sp_set_tuning": ([i32, i64], i32),
+        "sp_tma_eligible": ([i64, i64], i32),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+
+
+def load(path: str = LIB_PATH):
+    """Load (once) and return the ctypes library; raises if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise ImportError(
+                f"libsp200.so not found at {path}; build it with "
+                "`python -m paper_1006_3148_b200._build` (there is no CPU fallback)")
+        L = ctypes.CDLL(path)
+        _declare(L)
+        _lib = L
+    return _lib
+
+
+def check(rc: int, what: str = "") -> None:
+    """Map an sp200 status code to the reference's exception types."""
+    if rc == SP_OK:
+        return
+    msg = load().sp_last_error().decode(errors="replace")
+    if what:
+        msg = f"{what}: {msg}"
+    if rc == SP_EINVAL:
+        raise ValueError(msg)
+    if rc == SP_ERANGE:
+        raise IndexError(msg)
+    raise Sp200Error(msg)
+
+
+def launch_count(reset: bool = False) -> int:
+    return int(load().sp_launch_count(1 if reset else 0))

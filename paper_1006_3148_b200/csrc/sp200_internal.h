@@ -1,0 +1,34 @@
+// Host-side internals shared by the sp200 translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/sp200.h"
+
+namespace sp200 {
+
+// Per-thread error message + status helpers.
+int set_error(int code, const char *fmt, ...);
+int check_launch(const char *what);
+void count_launch(int n = 1);
+
+// Tuning table (sp_set_tuning).
+struct Tuning {
+    int64_t zchunk = 0;     // 0 = automatic
+    int64_t force_cpasync = 0;
+    int64_t cfg_index[SP_MAX_FUSED + 1] = {0, 0, 0, 0, 0};
+};
+Tuning &tuning();
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int sm_count();
+
+// Launchers implemented in sp200_temporal.cu.
+int launch_temporal(const double *src, double *dst, int64_t ex, int64_t ey, int64_t ez,
+                    int64_t nx, int64_t ny, int64_t nz, int64_t off, int levels, int64_t zlo,
+                    int64_t zhi, bool copy_ring, cudaStream_t stream);
+bool tma_eligible(const void *ptr, int64_t ex, int64_t ey);
+
+}  // namespace sp200

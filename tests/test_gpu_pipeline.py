@@ -1,0 +1,211 @@
+"""GPU parity: K2 fused temporally blocked passes and the run_pipelined /
+team_sweep / PipelineEngine drop-ins (mirrors pkg/tests/test_pipeline.py and
+acceptance criterion 1, tests/test_acceptance.py:59-85)."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import assert_bitwise
+
+pytestmark = pytest.mark.gpu
+
+sp = pytest.importorskip("paper_1006_3148_b200")
+
+
+def _cfg(**kw):
+    kw.setdefault("spec", sp.BlockSpec(12, 4, 4))
+    return sp.PipelineConfig(**kw)
+
+
+def _run(g0, cfg, passes):
+    if cfg.grid_mode == "compressed":
+        g = sp.create_grid(*g0.shape, pad=cfg.h)
+        g.interior_view().copy_(g0.interior_view())
+        g.capture_boundary_faces()
+        return sp.run_pipelined(g, cfg, passes)
+    return sp.run_pipelined((g0.copy(), g0.copy()), cfg, passes)
+
+
+def test_golden_pipelined_cases(golden):
+    for name, c in golden["pipelined"].items():
+        n = c["n"]
+        cfg = sp.PipelineConfig(spec=sp.BlockSpec(*c["spec"]), n=c["nteams"], t=c["t"], T=c["T"],
+                                d_l=1, d_u=c["d_u"], sync_mode=c["sync"], grid_mode=c["mode"])
+        if c["mode"] == "compressed":
+            g = sp.create_grid(n, n, n, pad=cfg.h, init="random", seed=c["seed"])
+            st = sp.run_pipelined(g, cfg, c["passes"])
+            assert st.result.alignment == 0
+        else:
+            a = sp.create_grid(n, n, n, init="random", seed=c["seed"])
+            st = sp.run_pipelined((a, a.copy()), cfg, c["passes"])
+        assert st.result.checksum() == c["digest"], name
+        assert st.updates_total == n ** 3 * c["sweeps"]
+
+
+@pytest.mark.parametrize("levels", [1, 2, 3, 4])
+@pytest.mark.parametrize("dims", [(60, 60, 60), (13, 9, 6), (70, 33, 17), (1, 5, 40), (130, 70, 20)])
+@pytest.mark.parametrize("loader", ["tma", "cpasync"])
+def test_fused_levels_equal_sweeps(levels, dims, loader):
+    L = sp._lib.load()
+    L.sp_set_tuning(1, 1 if loader == "cpasync" else 0)
+    try:
+        d0 = oracle.make_storage(*dims, init="random", seed=7, ring=0.75)
+        src = sp.Grid3.from_numpy(*dims, 0, d0)
+        dst = sp.Grid3.from_numpy(*dims, 0, np.full_like(d0, -3.0))
+        sp.fused_sweeps(src, dst, levels)
+        exp = oracle.interior(oracle.sweeps(d0, dims, levels), *dims)
+        assert_bitwise(dst.interior_numpy(), exp)
+        # ring untouched (two-grid pipeline never writes rings)
+        out = dst.to_numpy()
+        shell = np.ones_like(out, dtype=bool)
+        shell[1:-1, 1:-1, 1:-1] = False
+        assert np.all(out[shell] == -3.0)
+    finally:
+        L.sp_set_tuning(1, 0)
+
+
+@pytest.mark.parametrize("zc", [1, 2, 3, 7, 64])
+def test_fused_z_chunks(zc):
+    L = sp._lib.load()
+    L.sp_set_tuning(0, zc)
+    try:
+        dims = (40, 36, 45)
+        d0 = oracle.make_storage(*dims, init="random", seed=8)
+        exp = {t: oracle.interior(oracle.sweeps(d0, dims, t), *dims) for t in (1, 2, 3, 4)}
+        for t in (1, 2, 3, 4):
+            src = sp.Grid3.from_numpy(*dims, 0, d0)
+            dst = src.copy()
+            sp.fused_sweeps(src, dst, t)
+            assert_bitwise(dst.interior_numpy(), exp[t])
+    finally:
+        L.sp_set_tuning(0, 0)
+
+
+def test_fused_live_z_range_writes_only_range():
+    dims = (20, 20, 30)
+    d0 = oracle.make_storage(*dims, init="random", seed=2)
+    src = sp.Grid3.from_numpy(*dims, 0, d0)
+    dst = sp.Grid3.from_numpy(*dims, 0, np.full_like(d0, 9.0))
+    sp.fused_sweeps(src, dst, 3, zlo=4, zhi=25)
+    exp = oracle.interior(oracle.sweeps(d0, dims, 3), *dims)
+    got = dst.interior_numpy()
+    assert_bitwise(got[4:25], exp[4:25])
+    assert np.all(got[:4] == 9.0) and np.all(got[25:] == 9.0)
+
+
+@pytest.mark.parametrize("tune", [0, 1])
+def test_alternate_tile_configs(tune):
+    L = sp._lib.load()
+    for lv in (1, 2, 3, 4):
+        L.sp_set_tuning(2, lv * 16 + tune)
+    try:
+        dims = (100, 90, 33)
+        d0 = oracle.make_storage(*dims, init="random", seed=5, ring=1.0)
+        for t in (1, 2, 3, 4):
+            src = sp.Grid3.from_numpy(*dims, 0, d0)
+            dst = src.copy()
+            sp.fused_sweeps(src, dst, t)
+            assert_bitwise(dst.interior_numpy(), oracle.interior(oracle.sweeps(d0, dims, t), *dims))
+    finally:
+        for lv in (1, 2, 3, 4):
+            L.sp_set_tuning(2, lv * 16)
+
+
+def test_acceptance_matrix_60(oracle_cache):
+    """Criterion 1 (tests/test_acceptance.py:59-85): every (n,t,T,sync,mode,d_u)
+    equals n*t*T*passes reference sweeps bitwise."""
+    size, seed, passes = 60, 42, 2
+    base = sp.create_grid(size, size, size, init="random", seed=seed)
+    count = 0
+    for n in (1, 2):
+        for t in (1, 2, 3, 4):
+            for T in (1, 2):
+                for sync in ("relaxed", "barrier"):
+                    for mode in ("two_grid", "compressed"):
+                        cfg = sp.PipelineConfig(spec=sp.BlockSpec(60, 20, 20), n=n, t=t, T=T,
+                                                d_l=1, d_u=3, sync_mode=sync, grid_mode=mode)
+                        st = _run(base, cfg, passes)
+                        exp = oracle_cache.after_sweeps(size, seed, n * t * T * passes)
+                        assert_bitwise(st.result.interior_numpy(), exp)
+                        count += 1
+    assert count == 64
+
+
+def test_team_sweep_result_lands_in_reference_grid(oracle_cache):
+    g0 = sp.create_grid(60, 60, 60, init="random", seed=42)
+    for t in (1, 2, 3, 4, 5, 8):
+        a, b = g0.copy(), g0.copy()
+        cfg = _cfg(spec=sp.BlockSpec(60, 20, 20), t=t)
+        sp.team_sweep((a, b), cfg, 1)
+        holder = (a, b)[t % 2]  # reference: grids[h % 2]
+        assert_bitwise(holder.interior_numpy(), oracle_cache.after_sweeps(60, 42, t))
+
+
+def test_compressed_single_pass_realigned():
+    g0 = sp.create_grid(6, 6, 6, init="random", seed=33)
+    b = g0.copy()
+    sp.reference_sweep(g0, b)
+    cfg = sp.PipelineConfig(spec=sp.BlockSpec(6, 6, 6), grid_mode="compressed")
+    gc = sp.create_grid(6, 6, 6, pad=2, init="random", seed=33)
+    eng = sp.PipelineEngine(cfg, gc)
+    eng.run_pass(1)
+    assert gc.alignment == 1
+    assert_bitwise(gc.interior_numpy(), b.interior_numpy())
+
+
+def test_config_errors():
+    cfg = _cfg(grid_mode="compressed")
+    g = sp.create_grid(12, 12, 12, pad=1)
+    with pytest.raises(ValueError):
+        sp.run_pipelined(g, cfg, 3)
+    cfg = _cfg(n=1, t=2, T=1, grid_mode="compressed")
+    with pytest.raises(ValueError):
+        sp.run_pipelined(g, cfg, 2)
+    with pytest.raises(ValueError):
+        sp.PipelineEngine(_cfg(), (g,))
+    with pytest.raises(ValueError):
+        sp.PipelineEngine(_cfg(grid_mode="compressed"), (g, g.copy()))
+    with pytest.raises(ValueError):
+        sp.PipelineEngine(_cfg(spec=sp.BlockSpec(13, 4, 4)), (g, g.copy()))
+
+
+def test_unequal_rings_use_exact_per_level_path():
+    """Two-grid levels read the ring of grids[(lvl-1)%2] (sp/pipeline.py:301-308);
+    with different rings the engine must not fuse."""
+    n = 16
+    d0 = oracle.make_storage(n, n, n, init="random", seed=4)
+    d1 = d0.copy()
+    d1[0, :, :] = 2.0  # a different z-low ring in the second grid
+    a = sp.Grid3.from_numpy(n, n, n, 0, d0)
+    b = sp.Grid3.from_numpy(n, n, n, 0, d1)
+    cfg = _cfg(spec=sp.BlockSpec(16, 4, 4), t=3)
+    st = sp.run_pipelined((a, b), cfg, 1)
+    # reference emulation with the oracle
+    ga, gb = d0.copy(), d1.copy()
+    grids = [ga, gb]
+    for lvl in range(1, 4):
+        oracle.apply_window(grids[(lvl - 1) % 2], grids[lvl % 2], ((0, n), (0, n), (0, n)), 1, 1)
+    assert_bitwise(st.result.interior_numpy(), oracle.interior(grids[3 % 2], n, n, n))
+
+
+def test_large_config_c2_fused(golden):
+    c = golden["configs"]["C2"]
+    a = sp.create_grid(*c["n"], init="random", seed=c["seed"])
+    assert a.checksum() == c["init_digest"]
+    for t, passes in ((4, 25), (2, 50)):
+        g = a.copy()
+        cfg = sp.PipelineConfig(spec=sp.BlockSpec(512, 32, 32), t=t)
+        st = sp.run_pipelined((g, a.copy()), cfg, passes)
+        assert st.result.checksum() == c["digest"], t
+
+
+def test_large_config_c3_compressed(golden):
+    c = golden["configs"]["C3"]
+    g = sp.create_grid(*c["n"], pad=c["pad"], init="random", seed=c["seed"], lo=c["lo"], hi=c["hi"])
+    assert g.checksum() == c["init_digest"]
+    cfg = sp.PipelineConfig(spec=sp.BlockSpec(600, 30, 30), t=4, grid_mode="compressed")
+    st = sp.run_pipelined(g, cfg, 16)
+    assert st.result.alignment == 0
+    assert st.result.checksum() == c["digest"]
