@@ -44,27 +44,34 @@ struct TParams {
 template <int T, int WX, int CY, int R, int S>
 struct KCfg {
     static constexpr int CX = WX * 32;
-    static constexpr int PX = CX + 2, PY = CY + 2;
-    static constexpr int PLANE = PX * PY;
-    static constexpr int PLANE_AL = (PLANE + 15) & ~15;  // 128-byte aligned stages
+    static constexpr int PX = CX + 2, PY = CY + 2;  // region + 1-cell halo
+    // Stages hold CX+4 columns starting at an even x: TMA boxes must start on
+    // a 16-byte boundary, so an odd box origin is moved one column left and
+    // read back with a one-column shift (sh).
+    static constexpr int SPX = CX + 4;
+    static constexpr int SPLANE = SPX * PY;
+    static constexpr int SPLANE_AL = (SPLANE + 15) & ~15;  // 128-byte aligned stages
+    static constexpr int PLANE_AL = (PX * PY + 15) & ~15;   // level planes
     static constexpr int NT = WX * 32 * (CY / R);
     static constexpr int OX = CX - 2 * (T - 1), OY = CY - 2 * (T - 1);
     static constexpr int NLEV = (T > 1) ? 2 * (T - 1) : 0;
-    static constexpr size_t SMEM = (size_t)(S + NLEV) * PLANE_AL * sizeof(double) + 8 * S;
+    static constexpr size_t SMEM =
+        ((size_t)S * SPLANE_AL + (size_t)NLEV * PLANE_AL) * sizeof(double) + 8 * S;
     static_assert(CY % R == 0, "rows per thread must divide CY");
     static_assert(OX > 0 && OY > 0, "tile too small for the fused depth");
 };
 
 template <int T, int WX, int CY, int R, int S, bool TMA, bool RING>
-__global__ void __maxnreg__(224)
+__global__ void __launch_bounds__(KCfg<T, WX, CY, R, S>::NT, 1)
     k_temporal(const TParams p, const __grid_constant__ CUtensorMap tmap) {
     using C = KCfg<T, WX, CY, R, S>;
-    constexpr int PX = C::PX, PLANE = C::PLANE, PLANE_AL = C::PLANE_AL, NT = C::NT;
+    constexpr int PX = C::PX, SPX = C::SPX, SPLANE = C::SPLANE, SPLANE_AL = C::SPLANE_AL,
+                  PLANE_AL = C::PLANE_AL, NT = C::NT;
 
     extern __shared__ __align__(128) double sm[];
     double *stage = sm;
-    double *lev = sm + S * PLANE_AL;
-    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + (S + C::NLEV) * PLANE_AL);
+    double *lev = sm + S * SPLANE_AL;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(lev + C::NLEV * PLANE_AL);
 
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
@@ -91,18 +98,20 @@ __global__ void __maxnreg__(224)
     const int nload = (z1 - z0) + 2 * T;      // level-0 planes z0-T .. z1+T-1
     const int nsteps = (z1 - z0) + 3 * T - 1;  // level T emits plane z0+s-3T+1 at step s
     const int bx0 = rx0 - 1 + p.off, by0 = ry0 - 1 + p.off;
+    const int sh = bx0 & 1;  // stage column of storage x = bx0
+    const int bxs = bx0 - sh;
 
     auto issue = [&](int s) {
         const int si = s % S;
         const int zs = z0 - T + s + p.off;
         if constexpr (TMA) {
-            mbar_arrive_expect_tx(&bar[si], PLANE * 8);
-            tma_load_3d(stage + si * PLANE_AL, &tmap, &bar[si], bx0, by0, zs);
+            mbar_arrive_expect_tx(&bar[si], SPLANE * 8);
+            tma_load_3d(stage + si * SPLANE_AL, &tmap, &bar[si], bxs, by0, zs);
         } else {
-            double *dstage = stage + si * PLANE_AL;
+            double *dstage = stage + si * SPLANE_AL;
             const bool zok = (zs >= 0) && (zs < p.ez);
-            for (int q = tid; q < PLANE; q += NT) {
-                const int gx = bx0 + q % PX, gy = by0 + q / PX;
+            for (int q = tid; q < SPLANE; q += NT) {
+                const int gx = bxs + q % SPX, gy = by0 + q / SPX;
                 const bool inb = zok && gx >= 0 && gx < p.ex && gy >= 0 && gy < p.ey;
                 const double *g = inb ? p.src + ((int64_t)zs * p.ey + gy) * p.ex + gx : p.src;
                 cp_async_8(dstage + q, g, inb ? 8u : 0u);
@@ -152,7 +161,7 @@ __global__ void __maxnreg__(224)
             if (s + S - 1 < nload) issue(s + S - 1);
             else cp_async_commit();
         }
-        const double *cur = stage + si * PLANE_AL;
+        const double *cur = stage + si * SPLANE_AL + sh;
 
         if constexpr (RING) {
             // fused _copy_ring (sp/kernel.py:85-96): shell cells of this tile's box
@@ -161,11 +170,12 @@ __global__ void __maxnreg__(224)
             const bool zmid = (P0 >= z0) && (P0 < z1);
             if (s < nload && (zring || (zmid && ring_tile))) {
                 double *drow = p.dst + (int64_t)(P0 + p.off) * pz;
-                for (int q = tid; q < PLANE; q += NT) {
-                    const int gx = rx0 - 1 + q % PX, gy = ry0 - 1 + q / PX;
+                for (int q = tid; q < PX * C::PY; q += NT) {
+                    const int qx = q % PX, qy = q / PX;
+                    const int gx = rx0 - 1 + qx, gy = ry0 - 1 + qy;
                     if (gx < -1 || gx > p.nx || gy < -1 || gy > p.ny) continue;
                     const bool shell = zring || gx == -1 || gx == p.nx || gy == -1 || gy == p.ny;
-                    if (shell) drow[(int64_t)(gy + p.off) * p.ex + gx + p.off] = cur[q];
+                    if (shell) drow[(int64_t)(gy + p.off) * p.ex + gx + p.off] = cur[qy * SPX + qx];
                 }
             }
         }
@@ -176,16 +186,17 @@ __global__ void __maxnreg__(224)
             const int pout = pin - 1;                  // level u plane finished now
             const bool z_in = (pout >= 0) && (pout < p.nz);
             const double *B = (u == 1) ? cur : lev + ((u - 2) * 2 + ((s - 1) & 1)) * PLANE_AL;
+            const int pitch = (u == 1) ? SPX : PX;
             double w[R];
 #pragma unroll
             for (int r = 0; r < R; ++r)
-                w[r] = (u == 1) ? B[(j0 + r + 1) * PX + i + 1] : Pub[u - 2][r];
-            const double cm = B[j0 * PX + i + 1];
-            const double cp = B[(j0 + R + 1) * PX + i + 1];
+                w[r] = (u == 1) ? B[(j0 + r + 1) * pitch + i + 1] : Pub[u - 2][r];
+            const double cm = B[j0 * pitch + i + 1];
+            const double cp = B[(j0 + R + 1) * pitch + i + 1];
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                const double xm = B[(j0 + r + 1) * PX + i];
-                const double xp = B[(j0 + r + 1) * PX + i + 2];
+                const double xm = B[(j0 + r + 1) * pitch + i];
+                const double xp = B[(j0 + r + 1) * pitch + i + 2];
                 const double ym = (r == 0) ? cm : w[r - 1];
                 const double yp = (r == R - 1) ? cp : w[r + 1];
                 const double n = dadd(dadd(dadd(xm, xp), ym), yp);
@@ -313,7 +324,7 @@ static int launch_cfg(const double *src, double *dst, int64_t ex, int64_t ey, in
     if (use_tma) {
         cuuint64_t dims[3] = {(cuuint64_t)ex, (cuuint64_t)ey, (cuuint64_t)ez};
         cuuint64_t strides[2] = {(cuuint64_t)(ex * 8), (cuuint64_t)(ex * ey * 8)};
-        cuuint32_t box[3] = {(cuuint32_t)C::PX, (cuuint32_t)C::PY, 1};
+        cuuint32_t box[3] = {(cuuint32_t)C::SPX, (cuuint32_t)C::PY, 1};
         cuuint32_t estr[3] = {1, 1, 1};
         CUresult r = encode_fn()(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)src, dims,
                                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
