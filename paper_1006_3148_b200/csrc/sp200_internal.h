@@ -30,5 +30,8 @@ int launch_temporal(const double *src, double *dst, int64_t ex, int64_t ey, int6
                     int64_t nx, int64_t ny, int64_t nz, int64_t off, int levels, int64_t zlo,
                     int64_t zhi, bool copy_ring, cudaStream_t stream);
 bool tma_eligible(const void *ptr, int64_t ex, int64_t ey);
+int launch_sweep1(const double *src, double *dst, int64_t ex, int64_t ey, int64_t ez,
+                  int64_t nx, int64_t ny, int64_t nz, int64_t off, int64_t zlo, int64_t zhi,
+                  bool copy_ring, cudaStream_t stream);
 
 }  // namespace sp200

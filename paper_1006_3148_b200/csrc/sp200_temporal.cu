@@ -4,28 +4,31 @@
 // Dirichlet-ring copy of reference_sweep), K2 fuses T = 2..4 sweeps per HBM
 // pass.  Design (B200-first):
 //
-//  * A CTA owns an x-y tile and marches along z over a chunk of planes.  The
-//    level-0 input planes are staged by TMA (cp.async.bulk.tensor.3d, one
-//    elected thread, mbarrier completion) into an S-deep ring of shared-memory
-//    stages; a cp.async loader replaces TMA when the row pitch is not a
-//    multiple of 16 bytes.
-//  * Level u (1..T) is computed by the same thread for the same cells as level
-//    u-1, so the z-neighbour chain stays in registers: per cell and level the
-//    thread keeps the pending partial sum S = (((x-1 + x+1) + y-1) + y+1) + z-1
-//    and the previous plane's value; the +z+1 term and the x fl(1/6) finish the
-//    cell one plane later — exactly the reference order (sp/kernel.py:51-57).
-//  * In-plane neighbours of level u-1 come from shared memory: level u-1
-//    publishes each plane into a double-buffered smem plane, read by level u
-//    one step later (one __syncthreads per z step for all T levels).  A thread
-//    owns R consecutive rows of one column, so y-neighbours inside its rows
-//    come from registers.
-//  * Overlapped (ghost-zone) tiling: the CTA computes a CX x CY region at
-//    every level; the valid output shrinks by one cell per side per level, so
-//    the stored tile is (CX-2(T-1)) x (CY-2(T-1)).  Cells outside the interior
-//    (Dirichlet ring) keep their input value at every level.
+//  * A CTA owns a 64-column x CY-row region of an x-y tile and marches along
+//    z over a chunk of planes.  The level-0 input planes are staged by TMA
+//    (cp.async.bulk.tensor.3d issued by one thread, mbarrier completion) into
+//    an S-deep ring of shared-memory stages; a cp.async loader replaces TMA
+//    when the row pitch is not a multiple of 16 bytes.
+//  * One warp spans the 64 columns: lane l owns the column pair (2l, 2l+1) of
+//    R consecutive rows and computes those cells at every fused level, so the
+//    z-neighbour chain stays in registers: per cell and level the thread keeps
+//    the pending partial sum S = (((x-1 + x+1) + y-1) + y+1) + z-1; the +z+1
+//    term and the x fl(1/6) finish the cell one plane later — exactly the
+//    reference order (sp/kernel.py:51-57), no FMA contraction.
+//  * x-neighbours: the pair partner is in registers, the outer neighbours come
+//    from the adjacent lanes by warp shuffle; y-neighbours inside a thread's
+//    rows are registers.  Only each thread's first and last row is published
+//    to shared memory (double-buffered per level) for the y-neighbours of the
+//    adjacent row group — this keeps shared-memory traffic, the limiter of the
+//    fused pass, near 4 wavefronts per 32 cell-updates.
+//  * Overlapped (ghost-zone) tiling: the computed region shrinks by one valid
+//    cell per side per level; the stored tile is OX x (CY-2(T-1)).  Cells
+//    outside the interior (Dirichlet ring) keep their input value at every
+//    level.
 #include <string.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "sp200_device.cuh"
 #include "sp200_internal.h"
@@ -37,81 +40,110 @@ struct TParams {
     double *dst;
     int64_t ex, ey, ez;
     int nx, ny, nz, off;
+    int ox, ex0;   // stored tile width; region column of the first stored column
+    int pair_store;  // 16-byte aligned column pairs in global memory
     int tiles_x, ntiles;
     int zlo, zhi, zc;
 };
 
-template <int T, int WX, int CY, int R, int S>
+template <int T, int CY, int R, int S>
 struct KCfg {
-    static constexpr int CX = WX * 32;
-    static constexpr int PX = CX + 2, PY = CY + 2;  // region + 1-cell halo
-    // Stages hold CX+4 columns starting at an even x: TMA boxes must start on
-    // a 16-byte boundary, so an odd box origin is moved one column left and
-    // read back with a one-column shift (sh).
-    static constexpr int SPX = CX + 4;
-    static constexpr int SPLANE = SPX * PY;
-    static constexpr int SPLANE_AL = (SPLANE + 15) & ~15;  // 128-byte aligned stages
-    static constexpr int PLANE_AL = (PX * PY + 15) & ~15;   // level planes
-    static constexpr int NT = WX * 32 * (CY / R);
-    static constexpr int OX = CX - 2 * (T - 1), OY = CY - 2 * (T - 1);
+    static constexpr int CX = 64;                // region columns (one warp, 2 per lane)
+    static constexpr int PY = CY + 2;            // region rows + 1-row halo each side
+    static constexpr int SPX = CX + 4;           // stage / level row pitch (doubles)
+    static constexpr int C0 = 2;                 // smem column of region column 0
+    static constexpr int PLANE = SPX * PY;
+    static constexpr int PLANE_AL = (PLANE + 15) & ~15;  // 128-byte aligned planes
+    static constexpr int NT = 32 * (CY / R);
+    static constexpr int OY = CY - 2 * (T - 1);
     static constexpr int NLEV = (T > 1) ? 2 * (T - 1) : 0;
-    static constexpr size_t SMEM =
-        ((size_t)S * SPLANE_AL + (size_t)NLEV * PLANE_AL) * sizeof(double) + 8 * S;
+    static constexpr size_t SMEM = (size_t)(S + NLEV) * PLANE_AL * sizeof(double) + 8 * S;
     static_assert(CY % R == 0, "rows per thread must divide CY");
-    static_assert(OX > 0 && OY > 0, "tile too small for the fused depth");
+    static_assert(OY > 0, "tile too small for the fused depth");
 };
 
-template <int T, int WX, int CY, int R, int S, bool TMA, bool RING>
-__global__ void __launch_bounds__(KCfg<T, WX, CY, R, S>::NT, 1)
+template <int T, int R>
+struct LState {
+    double Sp[T][R][2];                     // pending partial sum of level u (index u-1)
+    double W0[2][R][2];                     // level-0 own values, by step parity
+    double P[T > 1 ? T - 1 : 1][2][R][2];   // outputs of levels 1..T-1, by step parity
+};
+
+template <int N>
+using IC = std::integral_constant<int, N>;
+
+__device__ __forceinline__ double2 lds2(const double *p) {
+    return *reinterpret_cast<const double2 *>(p);
+}
+__device__ __forceinline__ void sts2(double *p, double a, double b) {
+    *reinterpret_cast<double2 *>(p) = make_double2(a, b);
+}
+__device__ __forceinline__ void stg2_stream(double *p, double a, double b) {
+    __stcs(reinterpret_cast<double2 *>(p), make_double2(a, b));
+}
+
+template <int T, int CY, int R, int S, bool TMA, bool RING>
+__global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
     k_temporal(const TParams p, const __grid_constant__ CUtensorMap tmap) {
-    using C = KCfg<T, WX, CY, R, S>;
-    constexpr int PX = C::PX, SPX = C::SPX, SPLANE = C::SPLANE, SPLANE_AL = C::SPLANE_AL,
-                  PLANE_AL = C::PLANE_AL, NT = C::NT;
+    using C = KCfg<T, CY, R, S>;
+    constexpr int SPX = C::SPX, C0 = C::C0, PLANE = C::PLANE, PLANE_AL = C::PLANE_AL,
+                  NT = C::NT;
 
     extern __shared__ __align__(128) double sm[];
     double *stage = sm;
-    double *lev = sm + S * SPLANE_AL;
+    double *lev = sm + S * PLANE_AL;
     uint64_t *bar = reinterpret_cast<uint64_t *>(lev + C::NLEV * PLANE_AL);
 
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
-    const int i = (warp % WX) * 32 + lane;  // region column
-    const int j0 = (warp / WX) * R;         // first region row
+    const int i0 = 2 * lane;   // region column of this lane's first cell
+    const int j0 = warp * R;   // first region row
 
     const int tile = blockIdx.x % p.ntiles, chunk = blockIdx.x / p.ntiles;
-    const int x0 = (tile % p.tiles_x) * C::OX, y0 = (tile / p.tiles_x) * C::OY;
+    const int x0 = (tile % p.tiles_x) * p.ox, y0 = (tile / p.tiles_x) * C::OY;
     const int z0 = p.zlo + chunk * p.zc;
     const int z1 = min(z0 + p.zc, p.zhi);
-    const int rx0 = x0 - (T - 1), ry0 = y0 - (T - 1);
+    const int rx0 = x0 - p.ex0, ry0 = y0 - (T - 1);  // logical coords of region (0, 0)
 
-    const int x = rx0 + i;
-    const bool x_in = (x >= 0) && (x < p.nx);
-    const bool x_out = (i >= T - 1) && (i < T - 1 + C::OX) && (x < p.nx);
-    bool y_in[R], y_out[R];
+    bool x_out[2];
+    unsigned okb = 0;   // bit 2r+c: cell (row r, column c) is an interior cell in x and y
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const int xc = rx0 + i0 + c, ic = i0 + c;
+        x_out[c] = (ic >= p.ex0) && (ic < p.ex0 + p.ox) && (xc < p.nx);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int y = ry0 + j0 + r;
+            if (xc >= 0 && xc < p.nx && y >= 0 && y < p.ny) okb |= 1u << (2 * r + c);
+        }
+    }
+    bool y_out[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int jr = j0 + r, y = ry0 + jr;
-        y_in[r] = (y >= 0) && (y < p.ny);
         y_out[r] = (jr >= T - 1) && (jr < T - 1 + C::OY) && (y < p.ny);
     }
+    // warps whose cells are all interior in x and y skip the Dirichlet select
+    const bool wint = __all_sync(0xffffffffu, okb == (1u << (2 * R)) - 1u);
 
     const int nload = (z1 - z0) + 2 * T;      // level-0 planes z0-T .. z1+T-1
     const int nsteps = (z1 - z0) + 3 * T - 1;  // level T emits plane z0+s-3T+1 at step s
-    const int bx0 = rx0 - 1 + p.off, by0 = ry0 - 1 + p.off;
-    const int sh = bx0 & 1;  // stage column of storage x = bx0
-    const int bxs = bx0 - sh;
+    // storage x of stage column 0 (even: TMA boxes start on 16-byte boundaries)
+    const int bxs = rx0 + p.off - C0, bys = ry0 - 1 + p.off;
+    const int64_t pz = p.ex * p.ey;
+    double *dcol = p.dst + (int64_t)(ry0 + j0 + p.off) * p.ex + (rx0 + i0 + p.off);
 
     auto issue = [&](int s) {
         const int si = s % S;
         const int zs = z0 - T + s + p.off;
         if constexpr (TMA) {
-            mbar_arrive_expect_tx(&bar[si], SPLANE * 8);
-            tma_load_3d(stage + si * SPLANE_AL, &tmap, &bar[si], bxs, by0, zs);
+            mbar_arrive_expect_tx(&bar[si], PLANE * 8);
+            tma_load_3d(stage + si * PLANE_AL, &tmap, &bar[si], bxs, bys, zs);
         } else {
-            double *dstage = stage + si * SPLANE_AL;
+            double *dstage = stage + si * PLANE_AL;
             const bool zok = (zs >= 0) && (zs < p.ez);
-            for (int q = tid; q < SPLANE; q += NT) {
-                const int gx = bxs + q % SPX, gy = by0 + q / SPX;
+            for (int q = tid; q < PLANE; q += NT) {
+                const int gx = bxs + q % SPX, gy = bys + q / SPX;
                 const bool inb = zok && gx >= 0 && gx < p.ex && gy >= 0 && gy < p.ey;
                 const double *g = inb ? p.src + ((int64_t)zs * p.ey + gy) * p.ex + gx : p.src;
                 cp_async_8(dstage + q, g, inb ? 8u : 0u);
@@ -138,18 +170,100 @@ __global__ void __launch_bounds__(KCfg<T, WX, CY, R, S>::NT, 1)
         }
     }
 
-    // per level (index u-1): pending partial sum, previous plane value, and the
-    // last published value (input of level u+1)
-    double Sp[T][R], Wl[T][R], Pub[T][R];
+    LState<T, R> st;
 #pragma unroll
-    for (int u = 0; u < T; ++u)
+    for (int r = 0; r < R; ++r)
 #pragma unroll
-        for (int r = 0; r < R; ++r) Sp[u][r] = Wl[u][r] = Pub[u][r] = 0.0;
+        for (int c = 0; c < 2; ++c) {
+            st.W0[0][r][c] = st.W0[1][r][c] = 0.0;
+#pragma unroll
+            for (int u = 0; u < T; ++u) st.Sp[u][r][c] = 0.0;
+#pragma unroll
+            for (int u = 0; u < (T > 1 ? T - 1 : 1); ++u) st.P[u][0][r][c] = st.P[u][1][r][c] = 0.0;
+        }
 
-    const bool ring_tile = RING && (x0 == 0 || y0 == 0 || x0 + C::OX >= p.nx || y0 + C::OY >= p.ny);
-    const int64_t pz = p.ex * p.ey;
+    const bool ring_tile =
+        RING && (x0 == 0 || y0 == 0 || x0 + p.ox >= p.nx || y0 + C::OY >= p.ny);
 
-    for (int s = 0; s < nsteps; ++s) {
+    // All T levels advance one plane per step, deepest level first, so level u
+    // reads level u-1's previous-step outputs before level u-1 overwrites its
+    // older register set.  The step parity Q is a compile-time constant (the
+    // loop is unrolled by two) so the register rotation is pure renaming.
+    // MODE 0: every cell interior (no select); 1: static x/y Dirichlet mask;
+    // 2: mask plus per-level z-ring planes (domain z ends only).
+    auto levels = [&](int s, const double *cur, auto Qc, auto Mc) {
+        constexpr int Q = decltype(Qc)::value;
+        constexpr int MODE = decltype(Mc)::value;
+#pragma unroll
+        for (int u = T; u >= 1; --u) {
+            const int ui = (u > 1) ? u - 2 : 0;
+            const int pout = z0 - T + s - 2 * u + 1;
+            const bool z_in = (pout >= 0) && (pout < p.nz);
+            const double *B = (u == 1) ? cur : lev + ((u - 2) * 2 + (Q ^ 1)) * PLANE_AL;
+            if (u == 1) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const double2 a = lds2(B + (j0 + r + 1) * SPX + C0 + i0);
+                    st.W0[Q][r][0] = a.x;
+                    st.W0[Q][r][1] = a.y;
+                }
+            }
+            const double2 cm = lds2(B + j0 * SPX + C0 + i0);
+            const double2 cp = lds2(B + (j0 + R + 1) * SPX + C0 + i0);
+            double *pub = lev + ((u - 1) * 2 + Q) * PLANE_AL;
+            const bool store_plane = (u == T) && pout >= z0 && pout < z1;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                double A[2];
+                A[0] = (u == 1) ? st.W0[Q][r][0] : st.P[ui][Q ^ 1][r][0];
+                A[1] = (u == 1) ? st.W0[Q][r][1] : st.P[ui][Q ^ 1][r][1];
+                double left, right;
+                if (u == 1) {
+                    // level 0 lives in the stage: outer x-neighbours straight from smem
+                    left = B[(j0 + r + 1) * SPX + C0 + i0 - 1];
+                    right = B[(j0 + r + 1) * SPX + C0 + i0 + 2];
+                } else {
+                    left = __shfl_up_sync(0xffffffffu, A[1], 1);
+                    right = __shfl_down_sync(0xffffffffu, A[0], 1);
+                }
+                double out[2];
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const double w = A[c];
+                    const double xm = c ? A[0] : left;
+                    const double xp = c ? right : A[1];
+                    double ym, yp;
+                    if (r == 0) ym = c ? cm.y : cm.x;
+                    else ym = (u == 1) ? st.W0[Q][r > 0 ? r - 1 : 0][c] : st.P[ui][Q ^ 1][r > 0 ? r - 1 : 0][c];
+                    if (r == R - 1) yp = c ? cp.y : cp.x;
+                    else yp = (u == 1) ? st.W0[Q][r < R - 1 ? r + 1 : r][c] : st.P[ui][Q ^ 1][r < R - 1 ? r + 1 : r][c];
+                    const double wl = (u == 1) ? st.W0[Q ^ 1][r][c] : st.P[ui][Q][r][c];
+                    const double n = dadd(dadd(dadd(xm, xp), ym), yp);
+                    double v = dmul(dadd(st.Sp[u - 1][r][c], w), 1.0 / 6.0);
+                    if constexpr (MODE == 1) {
+                        if (!((okb >> (2 * r + c)) & 1u)) v = wl;
+                    } else if constexpr (MODE == 2) {
+                        if (!(((okb >> (2 * r + c)) & 1u) && z_in)) v = wl;
+                    }
+                    st.Sp[u - 1][r][c] = dadd(n, wl);
+                    out[c] = v;
+                    if (u < T) st.P[u < T ? u - 1 : 0][Q][r][c] = v;
+                }
+                if (u < T) {
+                    if (r == 0 || r == R - 1) sts2(pub + (j0 + r + 1) * SPX + C0 + i0, out[0], out[1]);
+                } else if (store_plane && y_out[r]) {
+                    double *g = dcol + (int64_t)(pout + p.off) * pz + (int64_t)r * p.ex;
+                    if (x_out[0] && x_out[1] && p.pair_store) stg2_stream(g, out[0], out[1]);
+                    else {
+                        if (x_out[0]) st_stream(g, out[0]);
+                        if (x_out[1]) st_stream(g + 1, out[1]);
+                    }
+                }
+            }
+        }
+    };
+
+    auto one_step = [&](int s, auto Qc) {
         const int si = s % S;
         if constexpr (TMA) {
             if (s < nload) mbar_wait(&bar[si], (uint32_t)((s / S) & 1));
@@ -161,7 +275,7 @@ __global__ void __launch_bounds__(KCfg<T, WX, CY, R, S>::NT, 1)
             if (s + S - 1 < nload) issue(s + S - 1);
             else cp_async_commit();
         }
-        const double *cur = stage + si * SPLANE_AL + sh;
+        const double *cur = stage + si * PLANE_AL;
 
         if constexpr (RING) {
             // fused _copy_ring (sp/kernel.py:85-96): shell cells of this tile's box
@@ -170,51 +284,27 @@ __global__ void __launch_bounds__(KCfg<T, WX, CY, R, S>::NT, 1)
             const bool zmid = (P0 >= z0) && (P0 < z1);
             if (s < nload && (zring || (zmid && ring_tile))) {
                 double *drow = p.dst + (int64_t)(P0 + p.off) * pz;
-                for (int q = tid; q < PX * C::PY; q += NT) {
-                    const int qx = q % PX, qy = q / PX;
-                    const int gx = rx0 - 1 + qx, gy = ry0 - 1 + qy;
+                for (int q = tid; q < PLANE; q += NT) {
+                    const int qx = q % SPX, qy = q / SPX;
+                    const int gx = rx0 - C0 + qx, gy = ry0 - 1 + qy;
+                    if (qx < C0 - 1 || qx > C0 + C::CX) continue;  // outside the region halo
                     if (gx < -1 || gx > p.nx || gy < -1 || gy > p.ny) continue;
                     const bool shell = zring || gx == -1 || gx == p.nx || gy == -1 || gy == p.ny;
-                    if (shell) drow[(int64_t)(gy + p.off) * p.ex + gx + p.off] = cur[qy * SPX + qx];
+                    if (shell) drow[(int64_t)(gy + p.off) * p.ex + gx + p.off] = cur[q];
                 }
             }
         }
+        // every level's finished plane inside [0, nz): no z-ring this step
+        const int pmax = z0 - T + s - 1, pmin = z0 - T + s - 2 * T + 1;
+        const bool zall = (pmin >= 0) && (pmax < p.nz);
+        if (wint && zall) levels(s, cur, Qc, IC<0>{});
+        else if (zall) levels(s, cur, Qc, IC<1>{});
+        else levels(s, cur, Qc, IC<2>{});
+    };
 
-#pragma unroll
-        for (int u = T; u >= 1; --u) {
-            const int pin = z0 - T + s - 2 * (u - 1);  // level u-1 plane consumed now
-            const int pout = pin - 1;                  // level u plane finished now
-            const bool z_in = (pout >= 0) && (pout < p.nz);
-            const double *B = (u == 1) ? cur : lev + ((u - 2) * 2 + ((s - 1) & 1)) * PLANE_AL;
-            const int pitch = (u == 1) ? SPX : PX;
-            double w[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r)
-                w[r] = (u == 1) ? B[(j0 + r + 1) * pitch + i + 1] : Pub[u - 2][r];
-            const double cm = B[j0 * pitch + i + 1];
-            const double cp = B[(j0 + R + 1) * pitch + i + 1];
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const double xm = B[(j0 + r + 1) * pitch + i];
-                const double xp = B[(j0 + r + 1) * pitch + i + 2];
-                const double ym = (r == 0) ? cm : w[r - 1];
-                const double yp = (r == R - 1) ? cp : w[r + 1];
-                const double n = dadd(dadd(dadd(xm, xp), ym), yp);
-                const double outv = (x_in && y_in[r] && z_in)
-                                        ? dmul(dadd(Sp[u - 1][r], w[r]), 1.0 / 6.0)
-                                        : Wl[u - 1][r];
-                Sp[u - 1][r] = dadd(n, Wl[u - 1][r]);
-                Wl[u - 1][r] = w[r];
-                if (u < T) {
-                    Pub[u - 1][r] = outv;
-                    lev[((u - 1) * 2 + (s & 1)) * PLANE_AL + (j0 + r + 1) * PX + i + 1] = outv;
-                } else if (x_out && y_out[r] && pout >= z0 && pout < z1) {
-                    st_stream(p.dst + (int64_t)(pout + p.off) * pz +
-                                  (int64_t)(ry0 + j0 + r + p.off) * p.ex + (x + p.off),
-                              outv);
-                }
-            }
-        }
+    for (int s = 0; s < nsteps; s += 2) {
+        one_step(s, IC<0>{});
+        if (s + 1 < nsteps) one_step(s + 1, IC<1>{});
     }
     if constexpr (!TMA) cp_async_wait<0>();
 }
@@ -250,12 +340,23 @@ bool tma_eligible(const void *ptr, int64_t ex, int64_t ey) {
     return true;
 }
 
-template <int T, int WX, int CY, int R, int S>
+template <int T, int CY, int R, int S>
 static int launch_cfg(const double *src, double *dst, int64_t ex, int64_t ey, int64_t ez,
                       int64_t nx, int64_t ny, int64_t nz, int64_t off, int64_t zlo, int64_t zhi,
                       bool copy_ring, cudaStream_t stream) {
-    using C = KCfg<T, WX, CY, R, S>;
-    const bool use_tma = !tuning().force_cpasync && tma_eligible(src, ex, ey) && encode_fn();
+    using C = KCfg<T, CY, R, S>;
+    // Pair alignment: region column 0 must sit at an even storage x (16-byte
+    // aligned pairs for LDS.128 / STG.128 and the TMA box origin).  Tiles
+    // start at multiples of the (even) stored width, so the parity of the
+    // region origin is the same for every tile: shift it by one column when
+    // needed and give up one stored column pair.
+    const bool aligned =
+        ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) % 16 == 0) &&
+        (ex % 2 == 0);
+    const int par = aligned ? (int)((off - (T - 1)) & 1) : 0;
+    const int ox = C::CX - 2 * (T - 1) - 2 * par;
+    const int ex0 = (T - 1) + par;
+    const bool use_tma = aligned && !tuning().force_cpasync && tma_eligible(src, ex, ey) && encode_fn();
 
     TParams p;
     p.src = src;
@@ -267,25 +368,18 @@ static int launch_cfg(const double *src, double *dst, int64_t ex, int64_t ey, in
     p.ny = (int)ny;
     p.nz = (int)nz;
     p.off = (int)off;
-    p.tiles_x = (int)((nx + C::OX - 1) / C::OX);
+    p.ox = ox;
+    p.ex0 = ex0;
+    p.pair_store = aligned ? 1 : 0;
+    p.tiles_x = (int)((nx + ox - 1) / ox);
     const int tiles_y = (int)((ny + C::OY - 1) / C::OY);
     p.ntiles = p.tiles_x * tiles_y;
     p.zlo = (int)zlo;
     p.zhi = (int)zhi;
 
     void (*kern)(const TParams, const CUtensorMap);
-    if constexpr (T == 1) {
-        if (use_tma)
-            kern = copy_ring ? k_temporal<T, WX, CY, R, S, true, true>
-                             : k_temporal<T, WX, CY, R, S, true, false>;
-        else
-            kern = copy_ring ? k_temporal<T, WX, CY, R, S, false, true>
-                             : k_temporal<T, WX, CY, R, S, false, false>;
-    } else {
-        if (copy_ring) return set_error(SP_EUNSUP, "ring copy is fused only into the plain sweep");
-        kern = use_tma ? k_temporal<T, WX, CY, R, S, true, false>
-                       : k_temporal<T, WX, CY, R, S, false, false>;
-    }
+    if (copy_ring) return set_error(SP_EUNSUP, "ring copy is fused only into the plain sweep");
+    kern = use_tma ? k_temporal<T, CY, R, S, true, false> : k_temporal<T, CY, R, S, false, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)C::SMEM);
     if (e != cudaSuccess)
@@ -340,31 +434,26 @@ static int launch_cfg(const double *src, double *dst, int64_t ex, int64_t ey, in
 int launch_temporal(const double *src, double *dst, int64_t ex, int64_t ey, int64_t ez,
                     int64_t nx, int64_t ny, int64_t nz, int64_t off, int levels, int64_t zlo,
                     int64_t zhi, bool copy_ring, cudaStream_t stream) {
+    if (levels == 1)
+        return launch_sweep1(src, dst, ex, ey, ez, nx, ny, nz, off, zlo, zhi, copy_ring, stream);
     const int idx = (int)tuning().cfg_index[levels];
-#define SP_L(T, WX, CY, R, S) \
-    return launch_cfg<T, WX, CY, R, S>(src, dst, ex, ey, ez, nx, ny, nz, off, zlo, zhi, copy_ring, stream)
+#define SP_L(T, CY, R, S) \
+    return launch_cfg<T, CY, R, S>(src, dst, ex, ey, ez, nx, ny, nz, off, zlo, zhi, copy_ring, stream)
     switch (levels) {
-    case 1:
-        switch (idx) {
-        case 1: SP_L(1, 2, 32, 4, 4);
-        case 2: SP_L(1, 1, 16, 2, 8);
-        case 3: SP_L(1, 2, 16, 1, 6);
-        default: SP_L(1, 2, 16, 2, 6);
-        }
     case 2:
         switch (idx) {
-        case 1: SP_L(2, 2, 64, 8, 3);
-        default: SP_L(2, 2, 32, 4, 4);
+        case 1: SP_L(2, 64, 8, 3);
+        default: SP_L(2, 32, 4, 4);
         }
     case 3:
         switch (idx) {
-        case 1: SP_L(3, 2, 48, 6, 3);
-        default: SP_L(3, 2, 32, 4, 3);
+        case 1: SP_L(3, 32, 2, 3);
+        default: SP_L(3, 32, 4, 3);
         }
     case 4:
         switch (idx) {
-        case 1: SP_L(4, 2, 24, 4, 3);
-        default: SP_L(4, 2, 32, 4, 3);
+        case 1: SP_L(4, 32, 2, 3);
+        default: SP_L(4, 32, 4, 3);
         }
     default:
         return set_error(SP_EUNSUP, "levels %d unsupported", levels);
