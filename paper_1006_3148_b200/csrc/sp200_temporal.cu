@@ -212,51 +212,70 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
             const double2 cp = lds2(B + (j0 + R + 1) * SPX + C0 + i0);
             double *pub = lev + ((u - 1) * 2 + Q) * PLANE_AL;
             const bool store_plane = (u == T) && pout >= z0 && pout < z1;
+            // gather the level u-1 inputs of all 2R cells first, then run the
+            // five dependent adds stage by stage across all cells so that the
+            // 8-cycle DADD latency is covered by independent work of this warp
+            double A[R][2], xl[R], xr[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                double A[2];
-                A[0] = (u == 1) ? st.W0[Q][r][0] : st.P[ui][Q ^ 1][r][0];
-                A[1] = (u == 1) ? st.W0[Q][r][1] : st.P[ui][Q ^ 1][r][1];
-                double left, right;
+                A[r][0] = (u == 1) ? st.W0[Q][r][0] : st.P[ui][Q ^ 1][r][0];
+                A[r][1] = (u == 1) ? st.W0[Q][r][1] : st.P[ui][Q ^ 1][r][1];
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
                 if (u == 1) {
                     // level 0 lives in the stage: outer x-neighbours straight from smem
-                    left = B[(j0 + r + 1) * SPX + C0 + i0 - 1];
-                    right = B[(j0 + r + 1) * SPX + C0 + i0 + 2];
+                    xl[r] = B[(j0 + r + 1) * SPX + C0 + i0 - 1];
+                    xr[r] = B[(j0 + r + 1) * SPX + C0 + i0 + 2];
                 } else {
-                    left = __shfl_up_sync(0xffffffffu, A[1], 1);
-                    right = __shfl_down_sync(0xffffffffu, A[0], 1);
+                    xl[r] = __shfl_up_sync(0xffffffffu, A[r][1], 1);
+                    xr[r] = __shfl_down_sync(0xffffffffu, A[r][0], 1);
                 }
-                double out[2];
+            }
+            double n[R][2], v[R][2];
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) v[r][c] = dadd(st.Sp[u - 1][r][c], A[r][c]);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                n[r][0] = dadd(xl[r], A[r][1]);
+                n[r][1] = dadd(A[r][0], xr[r]);
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+                    n[r][c] = dadd(n[r][c], (r == 0) ? (c ? cm.y : cm.x) : A[r > 0 ? r - 1 : 0][c]);
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+                    n[r][c] = dadd(n[r][c], (r == R - 1) ? (c ? cp.y : cp.x) : A[r < R - 1 ? r + 1 : r][c]);
+#pragma unroll
+            for (int r = 0; r < R; ++r)
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
-                    const double w = A[c];
-                    const double xm = c ? A[0] : left;
-                    const double xp = c ? right : A[1];
-                    double ym, yp;
-                    if (r == 0) ym = c ? cm.y : cm.x;
-                    else ym = (u == 1) ? st.W0[Q][r > 0 ? r - 1 : 0][c] : st.P[ui][Q ^ 1][r > 0 ? r - 1 : 0][c];
-                    if (r == R - 1) yp = c ? cp.y : cp.x;
-                    else yp = (u == 1) ? st.W0[Q][r < R - 1 ? r + 1 : r][c] : st.P[ui][Q ^ 1][r < R - 1 ? r + 1 : r][c];
                     const double wl = (u == 1) ? st.W0[Q ^ 1][r][c] : st.P[ui][Q][r][c];
-                    const double n = dadd(dadd(dadd(xm, xp), ym), yp);
-                    double v = dmul(dadd(st.Sp[u - 1][r][c], w), 1.0 / 6.0);
+                    v[r][c] = dmul(v[r][c], 1.0 / 6.0);
                     if constexpr (MODE == 1) {
-                        if (!((okb >> (2 * r + c)) & 1u)) v = wl;
+                        if (!((okb >> (2 * r + c)) & 1u)) v[r][c] = wl;
                     } else if constexpr (MODE == 2) {
-                        if (!(((okb >> (2 * r + c)) & 1u) && z_in)) v = wl;
+                        if (!(((okb >> (2 * r + c)) & 1u) && z_in)) v[r][c] = wl;
                     }
-                    st.Sp[u - 1][r][c] = dadd(n, wl);
-                    out[c] = v;
-                    if (u < T) st.P[u < T ? u - 1 : 0][Q][r][c] = v;
+                    st.Sp[u - 1][r][c] = dadd(n[r][c], wl);
+                    if (u < T) st.P[u < T ? u - 1 : 0][Q][r][c] = v[r][c];
                 }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
                 if (u < T) {
-                    if (r == 0 || r == R - 1) sts2(pub + (j0 + r + 1) * SPX + C0 + i0, out[0], out[1]);
+                    if (r == 0 || r == R - 1) sts2(pub + (j0 + r + 1) * SPX + C0 + i0, v[r][0], v[r][1]);
                 } else if (store_plane && y_out[r]) {
                     double *g = dcol + (int64_t)(pout + p.off) * pz + (int64_t)r * p.ex;
-                    if (x_out[0] && x_out[1] && p.pair_store) stg2_stream(g, out[0], out[1]);
+                    if (x_out[0] && x_out[1] && p.pair_store) stg2_stream(g, v[r][0], v[r][1]);
                     else {
-                        if (x_out[0]) st_stream(g, out[0]);
-                        if (x_out[1]) st_stream(g + 1, out[1]);
+                        if (x_out[0]) st_stream(g, v[r][0]);
+                        if (x_out[1]) st_stream(g + 1, v[r][1]);
                     }
                 }
             }
@@ -442,18 +461,19 @@ int launch_temporal(const double *src, double *dst, int64_t ex, int64_t ey, int6
     switch (levels) {
     case 2:
         switch (idx) {
-        case 1: SP_L(2, 64, 8, 3);
-        default: SP_L(2, 32, 4, 4);
+        case 1: SP_L(2, 32, 4, 4);
+        default: SP_L(2, 32, 4, 6);
         }
     case 3:
         switch (idx) {
-        case 1: SP_L(3, 32, 2, 3);
-        default: SP_L(3, 32, 4, 3);
+        case 1: SP_L(3, 32, 4, 3);
+        default: SP_L(3, 32, 4, 5);
         }
     case 4:
         switch (idx) {
-        case 1: SP_L(4, 32, 2, 3);
-        default: SP_L(4, 32, 4, 3);
+        case 1: SP_L(4, 32, 4, 3);
+        case 2: SP_L(4, 32, 4, 5);
+        default: SP_L(4, 32, 4, 4);
         }
     default:
         return set_error(SP_EUNSUP, "levels %d unsupported", levels);
