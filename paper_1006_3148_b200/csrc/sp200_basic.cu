@@ -454,18 +454,35 @@ int sp_temporal(const double *src, double *dst, int64_t ex, int64_t ey, int64_t 
 int sp_tma_eligible(int64_t ex, int64_t ey) { return tma_eligible(nullptr, ex, ey) ? 1 : 0; }
 
 int64_t sp_compressed_workspace(int64_t nx, int64_t ny, int64_t nz, int levels) {
-    (void)nx; (void)ny; (void)nz; (void)levels;
-    return 0;
+    (void)nz;
+    if (nx < 1 || ny < 1 || levels < 1 || levels > SP_MAX_FUSED) return 0;
+    return compressed_workspace(nx, ny, levels);
 }
 
 int sp_compressed(double *data, int64_t ex, int64_t ey, int64_t ez, int64_t nx, int64_t ny,
                   int64_t nz, int64_t src_off, int direction, int levels, int64_t zlo,
                   int64_t zhi, void *flags, const double *const faces[6], int side_mask,
                   void *stream) {
-    (void)data; (void)ex; (void)ey; (void)ez; (void)nx; (void)ny; (void)nz; (void)src_off;
-    (void)direction; (void)levels; (void)zlo; (void)zhi; (void)flags; (void)faces;
-    (void)side_mask; (void)stream;
-    return set_error(SP_EUNSUP, "sp_compressed: fused compressed pass not built yet");
+    if (!data || !flags) return set_error(SP_EINVAL, "null argument");
+    if (direction != 1 && direction != -1) return set_error(SP_EINVAL, "direction must be +1 or -1");
+    if (levels < 1 || levels > SP_MAX_FUSED)
+        return set_error(SP_EUNSUP, "levels %d outside [1, %d]", levels, SP_MAX_FUSED);
+    int rc = check_geom(ex, ey, ez, nx, ny, nz, src_off);
+    if (rc) return rc;
+    const int64_t doff = src_off - (direction > 0 ? levels : -levels);
+    rc = check_geom(ex, ey, ez, nx, ny, nz, doff);
+    if (rc) return set_error(SP_EINVAL, "shifted frame (offset %lld) leaves the padded storage",
+                             (long long)doff);
+    if (zlo < 0) zlo = 0;
+    if (zhi > nz) zhi = nz;
+    if (zlo < zhi) {
+        rc = launch_compressed(data, ex, ey, ez, nx, ny, nz, src_off, direction, levels, zlo, zhi,
+                               flags, as_stream(stream));
+        if (rc) return rc;
+    }
+    if (faces && side_mask) return sp_write_faces(data, ex, ey, ez, nx, ny, nz, doff, faces,
+                                                  side_mask, stream);
+    return SP_OK;
 }
 
 }  // extern "C"

@@ -42,8 +42,12 @@ struct TParams {
     int nx, ny, nz, off;
     int ox, ex0;   // stored tile width; region column of the first stored column
     int pair_store;  // 16-byte aligned column pairs in global memory
-    int tiles_x, ntiles;
+    int tiles_x, tiles_y, ntiles;
     int zlo, zhi, zc;
+    int doff;        // storage offset of logical 0 in the written frame
+    int direction;   // K3: +1 forward (write shifted -T), -1 backward
+    int *ticket;     // K3: tile ticket counter
+    unsigned *prog;  // K3: per-tile progress (input planes delivered)
 };
 
 template <int T, int CY, int R, int S>
@@ -57,7 +61,7 @@ struct KCfg {
     static constexpr int NT = 32 * (CY / R);
     static constexpr int OY = CY - 2 * (T - 1);
     static constexpr int NLEV = (T > 1) ? 2 * (T - 1) : 0;
-    static constexpr size_t SMEM = (size_t)(S + NLEV) * PLANE_AL * sizeof(double) + 8 * S;
+    static constexpr size_t SMEM = (size_t)(S + NLEV) * PLANE_AL * sizeof(double) + 8 * S + 16;
     static_assert(CY % R == 0, "rows per thread must divide CY");
     static_assert(OY > 0, "tile too small for the fused depth");
 };
@@ -82,7 +86,16 @@ __device__ __forceinline__ void stg2_stream(double *p, double a, double b) {
     __stcs(reinterpret_cast<double2 *>(p), make_double2(a, b));
 }
 
-template <int T, int CY, int R, int S, bool TMA, bool RING>
+// COMP: the compressed single-array pass (K3).  Reads the level-0 frame at
+// p.off and writes level T into the same array at p.doff = p.off -/+ T.  The
+// write of a tile lands in the read regions of its lower (forward) / upper
+// (backward) x-y neighbours, so tiles are taken in that order from a global
+// ticket counter and a tile publishes, per z step, how many input planes its
+// TMA loads have delivered; before storing plane Q a tile waits until its
+// three predecessor tiles have loaded plane Q -/+ T.  Predecessors hold
+// smaller tickets, so they are resident or done: the wait cannot deadlock.
+// This is the paper's relaxed pipeline synchronisation (Eq. 3) between CTAs.
+template <int T, int CY, int R, int S, bool TMA, bool COMP>
 __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
     k_temporal(const TParams p, const __grid_constant__ CUtensorMap tmap) {
     using C = KCfg<T, CY, R, S>;
@@ -93,16 +106,63 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
     double *stage = sm;
     double *lev = sm + S * PLANE_AL;
     uint64_t *bar = reinterpret_cast<uint64_t *>(lev + C::NLEV * PLANE_AL);
+    int *tile_slot = reinterpret_cast<int *>(bar + S);
 
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     const int i0 = 2 * lane;   // region column of this lane's first cell
     const int j0 = warp * R;   // first region row
 
-    const int tile = blockIdx.x % p.ntiles, chunk = blockIdx.x / p.ntiles;
-    const int x0 = (tile % p.tiles_x) * p.ox, y0 = (tile / p.tiles_x) * C::OY;
-    const int z0 = p.zlo + chunk * p.zc;
-    const int z1 = min(z0 + p.zc, p.zhi);
+    if constexpr (TMA) {
+        if (tid == 0) {
+            tma_prefetch_desc(&tmap);
+#pragma unroll
+            for (int si = 0; si < S; ++si) mbar_init(&bar[si], 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+    }
+
+    LState<T, R> st;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            st.W0[0][r][c] = st.W0[1][r][c] = 0.0;
+#pragma unroll
+            for (int u = 0; u < T; ++u) st.Sp[u][r][c] = 0.0;
+#pragma unroll
+            for (int u = 0; u < (T > 1 ? T - 1 : 1); ++u) st.P[u][0][r][c] = st.P[u][1][r][c] = 0.0;
+        }
+
+    uint32_t gbase = 0;  // stage loads issued by this CTA before the current unit
+    for (int unit = 0;; ++unit) {
+    int tile, z0, z1;
+    if constexpr (COMP) {
+        // persistent CTAs, tickets in predecessor-first order
+        if (tid == 0) {
+            const int t = atomicAdd(p.ticket, 1);
+            *tile_slot = t;
+        }
+        __syncthreads();
+        const int t = *tile_slot;
+        __syncthreads();
+        if (t >= p.ntiles) break;
+        tile = (p.direction > 0) ? t : p.ntiles - 1 - t;
+        z0 = p.zlo;
+        z1 = p.zhi;
+    } else {
+        if (unit > 0) break;
+        // one (tile, z-chunk) unit per CTA, tile-fastest so that concurrently
+        // running CTAs cover neighbouring tiles at the same z range and the
+        // overlapped halo reads hit L2
+        tile = blockIdx.x % p.ntiles;
+        const int chunk = blockIdx.x / p.ntiles;
+        z0 = p.zlo + chunk * p.zc;
+        z1 = min(z0 + p.zc, p.zhi);
+    }
+    const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
+    const int x0 = tx * p.ox, y0 = ty * C::OY;
     const int rx0 = x0 - p.ex0, ry0 = y0 - (T - 1);  // logical coords of region (0, 0)
 
     bool x_out[2];
@@ -131,10 +191,16 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
     // storage x of stage column 0 (even: TMA boxes start on 16-byte boundaries)
     const int bxs = rx0 + p.off - C0, bys = ry0 - 1 + p.off;
     const int64_t pz = p.ex * p.ey;
-    double *dcol = p.dst + (int64_t)(ry0 + j0 + p.off) * p.ex + (rx0 + i0 + p.off);
+    double *dcol = p.dst + (int64_t)(ry0 + j0 + p.doff) * p.ex + (rx0 + i0 + p.doff);
+
+    // K3 predecessor tiles (forward: x-1, y-1, both; backward: x+1, y+1, both)
+    const int dxn = (p.direction > 0) ? -1 : 1;
+    const bool hx = COMP && (tx + dxn >= 0) && (tx + dxn < p.tiles_x);
+    const bool hy = COMP && (ty + dxn >= 0) && (ty + dxn < p.tiles_y);
+    const int tpx = tile + dxn, tpy = tile + dxn * p.tiles_x, tpxy = tile + dxn * (p.tiles_x + 1);
 
     auto issue = [&](int s) {
-        const int si = s % S;
+        const int si = (int)((gbase + s) % S);
         const int zs = z0 - T + s + p.off;
         if constexpr (TMA) {
             mbar_arrive_expect_tx(&bar[si], PLANE * 8);
@@ -153,13 +219,6 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
     };
 
     if constexpr (TMA) {
-        if (tid == 0) {
-            tma_prefetch_desc(&tmap);
-#pragma unroll
-            for (int si = 0; si < S; ++si) mbar_init(&bar[si], 1);
-            fence_mbar_init();
-        }
-        __syncthreads();
         if (tid == 0)
             for (int s = 0; s < S - 1; ++s)
                 if (s < nload) issue(s);
@@ -169,21 +228,6 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
             else cp_async_commit();
         }
     }
-
-    LState<T, R> st;
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            st.W0[0][r][c] = st.W0[1][r][c] = 0.0;
-#pragma unroll
-            for (int u = 0; u < T; ++u) st.Sp[u][r][c] = 0.0;
-#pragma unroll
-            for (int u = 0; u < (T > 1 ? T - 1 : 1); ++u) st.P[u][0][r][c] = st.P[u][1][r][c] = 0.0;
-        }
-
-    const bool ring_tile =
-        RING && (x0 == 0 || y0 == 0 || x0 + p.ox >= p.nx || y0 + C::OY >= p.ny);
 
     // All T levels advance one plane per step, deepest level first, so level u
     // reads level u-1's previous-step outputs before level u-1 overwrites its
@@ -271,7 +315,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
                 if (u < T) {
                     if (r == 0 || r == R - 1) sts2(pub + (j0 + r + 1) * SPX + C0 + i0, v[r][0], v[r][1]);
                 } else if (store_plane && y_out[r]) {
-                    double *g = dcol + (int64_t)(pout + p.off) * pz + (int64_t)r * p.ex;
+                    double *g = dcol + (int64_t)(pout + p.doff) * pz + (int64_t)r * p.ex;
                     if (x_out[0] && x_out[1] && p.pair_store) stg2_stream(g, v[r][0], v[r][1]);
                     else {
                         if (x_out[0]) st_stream(g, v[r][0]);
@@ -283,36 +327,36 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
     };
 
     auto one_step = [&](int s, auto Qc) {
-        const int si = s % S;
+        const int si = (int)((gbase + s) % S);
         if constexpr (TMA) {
-            if (s < nload) mbar_wait(&bar[si], (uint32_t)((s / S) & 1));
-            __syncthreads();
-            if (tid == 0 && s + S - 1 < nload) issue(s + S - 1);
+            if (s < nload) mbar_wait(&bar[si], (uint32_t)(((gbase + s) / S) & 1));
         } else {
             cp_async_wait<S - 2>();
-            __syncthreads();
+        }
+        if constexpr (COMP) {
+            if (tid == 0) {
+                // publish: input planes of this tile delivered so far
+                st_release_gpu(p.prog + tile, (unsigned)(s + 1));
+                // before this step stores plane Q = z0+s-3T+1 (frame shift
+                // -/+T), the predecessors must have loaded input plane Q -/+ T,
+                // i.e. completed their step s-3T+1 (and, for the backward pass,
+                // 2T further)
+                const int need = s - 3 * T + 2 + ((p.direction > 0) ? 0 : 2 * T);
+                if (need > 0) {
+                    if (hx) while ((int)ld_acquire_gpu(p.prog + tpx) < need) __nanosleep(64);
+                    if (hy) while ((int)ld_acquire_gpu(p.prog + tpy) < need) __nanosleep(64);
+                    if (hx && hy) while ((int)ld_acquire_gpu(p.prog + tpxy) < need) __nanosleep(64);
+                }
+            }
+        }
+        __syncthreads();
+        if constexpr (TMA) {
+            if (tid == 0 && s + S - 1 < nload) issue(s + S - 1);
+        } else {
             if (s + S - 1 < nload) issue(s + S - 1);
             else cp_async_commit();
         }
         const double *cur = stage + si * PLANE_AL;
-
-        if constexpr (RING) {
-            // fused _copy_ring (sp/kernel.py:85-96): shell cells of this tile's box
-            const int P0 = z0 - T + s;
-            const bool zring = (P0 == -1 && z0 == 0) || (P0 == p.nz && z1 == p.nz);
-            const bool zmid = (P0 >= z0) && (P0 < z1);
-            if (s < nload && (zring || (zmid && ring_tile))) {
-                double *drow = p.dst + (int64_t)(P0 + p.off) * pz;
-                for (int q = tid; q < PLANE; q += NT) {
-                    const int qx = q % SPX, qy = q / SPX;
-                    const int gx = rx0 - C0 + qx, gy = ry0 - 1 + qy;
-                    if (qx < C0 - 1 || qx > C0 + C::CX) continue;  // outside the region halo
-                    if (gx < -1 || gx > p.nx || gy < -1 || gy > p.ny) continue;
-                    const bool shell = zring || gx == -1 || gx == p.nx || gy == -1 || gy == p.ny;
-                    if (shell) drow[(int64_t)(gy + p.off) * p.ex + gx + p.off] = cur[q];
-                }
-            }
-        }
         // every level's finished plane inside [0, nz): no z-ring this step
         const int pmax = z0 - T + s - 1, pmin = z0 - T + s - 2 * T + 1;
         const bool zall = (pmin >= 0) && (pmax < p.nz);
@@ -326,6 +370,12 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
         if (s + 1 < nsteps) one_step(s + 1, IC<1>{});
     }
     if constexpr (!TMA) cp_async_wait<0>();
+    if constexpr (COMP) {
+        __syncthreads();
+        if (tid == 0) st_release_gpu(p.prog + tile, 0x7fffffffu);  // tile done
+    }
+    gbase += (uint32_t)nload;
+    }  // units
 }
 
 // ---------------------------------------------------------------------------
@@ -359,95 +409,153 @@ bool tma_eligible(const void *ptr, int64_t ex, int64_t ey) {
     return true;
 }
 
+struct LaunchReq {
+    const double *src;
+    double *dst;
+    int64_t ex, ey, ez, nx, ny, nz, off, doff, zlo, zhi;
+    int direction;  // 0: two-grid (K1/K2); +1/-1: compressed in place (K3)
+    void *ws;       // K3 workspace (ticket + per-tile progress)
+    cudaStream_t stream;
+};
+
+template <int T, int CY>
+static int tile_geometry(int64_t nx, int64_t ny, int64_t off, bool aligned, int *ox, int *ex0,
+                         int *tiles_x, int *tiles_y) {
+    using C = KCfg<T, CY, 4, 4>;
+    const int par = aligned ? (int)((off - (T - 1)) & 1) : 0;
+    *ox = C::CX - 2 * (T - 1) - 2 * par;
+    *ex0 = (T - 1) + par;
+    *tiles_x = (int)((nx + *ox - 1) / *ox);
+    *tiles_y = (int)((ny + C::OY - 1) / C::OY);
+    return par;
+}
+
 template <int T, int CY, int R, int S>
-static int launch_cfg(const double *src, double *dst, int64_t ex, int64_t ey, int64_t ez,
-                      int64_t nx, int64_t ny, int64_t nz, int64_t off, int64_t zlo, int64_t zhi,
-                      bool copy_ring, cudaStream_t stream) {
+static int launch_cfg(const LaunchReq &q) {
     using C = KCfg<T, CY, R, S>;
+    const bool comp = q.direction != 0;
     // Pair alignment: region column 0 must sit at an even storage x (16-byte
     // aligned pairs for LDS.128 / STG.128 and the TMA box origin).  Tiles
     // start at multiples of the (even) stored width, so the parity of the
     // region origin is the same for every tile: shift it by one column when
     // needed and give up one stored column pair.
     const bool aligned =
-        ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) % 16 == 0) &&
-        (ex % 2 == 0);
-    const int par = aligned ? (int)((off - (T - 1)) & 1) : 0;
-    const int ox = C::CX - 2 * (T - 1) - 2 * par;
-    const int ex0 = (T - 1) + par;
-    const bool use_tma = aligned && !tuning().force_cpasync && tma_eligible(src, ex, ey) && encode_fn();
-
+        ((reinterpret_cast<uintptr_t>(q.dst) | reinterpret_cast<uintptr_t>(q.src)) % 16 == 0) &&
+        (q.ex % 2 == 0);
     TParams p;
-    p.src = src;
-    p.dst = dst;
-    p.ex = ex;
-    p.ey = ey;
-    p.ez = ez;
-    p.nx = (int)nx;
-    p.ny = (int)ny;
-    p.nz = (int)nz;
-    p.off = (int)off;
-    p.ox = ox;
-    p.ex0 = ex0;
-    p.pair_store = aligned ? 1 : 0;
-    p.tiles_x = (int)((nx + ox - 1) / ox);
-    const int tiles_y = (int)((ny + C::OY - 1) / C::OY);
+    int tiles_y;
+    tile_geometry<T, CY>(q.nx, q.ny, q.off, aligned, &p.ox, &p.ex0, &p.tiles_x, &tiles_y);
+    const bool use_tma =
+        aligned && !tuning().force_cpasync && tma_eligible(q.src, q.ex, q.ey) && encode_fn();
+    p.src = q.src;
+    p.dst = q.dst;
+    p.ex = q.ex;
+    p.ey = q.ey;
+    p.ez = q.ez;
+    p.nx = (int)q.nx;
+    p.ny = (int)q.ny;
+    p.nz = (int)q.nz;
+    p.off = (int)q.off;
+    p.doff = (int)q.doff;
+    p.direction = q.direction;
+    p.pair_store = (aligned && ((q.off - q.doff) % 2 == 0)) ? 1 : 0;
+    p.tiles_y = tiles_y;
     p.ntiles = p.tiles_x * tiles_y;
-    p.zlo = (int)zlo;
-    p.zhi = (int)zhi;
+    p.zlo = (int)q.zlo;
+    p.zhi = (int)q.zhi;
+    p.ticket = nullptr;
+    p.prog = nullptr;
 
     void (*kern)(const TParams, const CUtensorMap);
-    if (copy_ring) return set_error(SP_EUNSUP, "ring copy is fused only into the plain sweep");
-    kern = use_tma ? k_temporal<T, CY, R, S, true, false> : k_temporal<T, CY, R, S, false, false>;
+    if (comp)
+        kern = use_tma ? k_temporal<T, CY, R, S, true, true> : k_temporal<T, CY, R, S, false, true>;
+    else
+        kern = use_tma ? k_temporal<T, CY, R, S, true, false> : k_temporal<T, CY, R, S, false, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)C::SMEM);
     if (e != cudaSuccess)
         return set_error(SP_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
 
-    // z-chunking: choose the chunk count minimising (waves x steps per chunk)
-    const int64_t depth = zhi - zlo;
+    const int64_t depth = q.zhi - q.zlo;
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::NT, C::SMEM);
     if (occ < 1) occ = 1;
     const int64_t slots = (int64_t)sm_count() * occ;
-    int64_t zc = tuning().zchunk;
-    if (zc <= 0) {
-        double best = 1e300;
-        for (int64_t c = 1; c <= 256 && c <= depth; ++c) {
-            int64_t len = (depth + c - 1) / c;
-            int64_t units = p.ntiles * ((depth + len - 1) / len);
-            double waves = (double)((units + slots - 1) / slots);
-            // partial last wave still costs a whole wave; a short chunk pays the
-            // (3T-1)-step pipeline fill/drain and the 2T-plane halo reload
-            double cost = waves * (double)(len + 3 * T - 1 + (T == 1 ? 1 : 0));
-            if (cost < best * 0.999) {
-                best = cost;
-                zc = len;
+    int64_t grid;
+    if (comp) {
+        // persistent CTAs walking full columns in ticket order
+        p.zc = (int)depth;
+        grid = std::min<int64_t>(slots, p.ntiles);
+        p.ticket = reinterpret_cast<int *>(q.ws);
+        p.prog = reinterpret_cast<unsigned *>(reinterpret_cast<char *>(q.ws) + 128);
+        e = cudaMemsetAsync(q.ws, 0, 128 + (size_t)p.ntiles * 4, q.stream);
+        if (e != cudaSuccess)
+            return set_error(SP_ECUDA, "cudaMemsetAsync: %s", cudaGetErrorString(e));
+    } else {
+        // z-chunking: choose the chunk count minimising (waves x steps per chunk)
+        int64_t zc = tuning().zchunk;
+        if (zc <= 0) {
+            double best = 1e300;
+            for (int64_t c = 1; c <= 256 && c <= depth; ++c) {
+                int64_t len = (depth + c - 1) / c;
+                int64_t units = p.ntiles * ((depth + len - 1) / len);
+                double waves = (double)((units + slots - 1) / slots);
+                // a partial last wave still costs a whole wave; a short chunk
+                // pays the (3T-1)-step pipeline fill/drain
+                double cost = waves * (double)(len + 3 * T - 1);
+                if (cost < best * 0.999) {
+                    best = cost;
+                    zc = len;
+                }
             }
         }
+        if (zc < 1) zc = 1;
+        p.zc = (int)zc;
+        grid = (int64_t)p.ntiles * ((depth + zc - 1) / zc);
     }
-    if (zc < 1) zc = 1;
-    p.zc = (int)zc;
-    const int64_t nchunks = (depth + zc - 1) / zc;
-    const int64_t grid = (int64_t)p.ntiles * nchunks;
     if (grid > 0x7fffffff) return set_error(SP_EUNSUP, "grid too large");
 
     CUtensorMap tmap;
     memset(&tmap, 0, sizeof(tmap));
     if (use_tma) {
-        cuuint64_t dims[3] = {(cuuint64_t)ex, (cuuint64_t)ey, (cuuint64_t)ez};
-        cuuint64_t strides[2] = {(cuuint64_t)(ex * 8), (cuuint64_t)(ex * ey * 8)};
+        cuuint64_t dims[3] = {(cuuint64_t)q.ex, (cuuint64_t)q.ey, (cuuint64_t)q.ez};
+        cuuint64_t strides[2] = {(cuuint64_t)(q.ex * 8), (cuuint64_t)(q.ex * q.ey * 8)};
         cuuint32_t box[3] = {(cuuint32_t)C::SPX, (cuuint32_t)C::PY, 1};
         cuuint32_t estr[3] = {1, 1, 1};
-        CUresult r = encode_fn()(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)src, dims,
+        CUresult r = encode_fn()(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)q.src, dims,
                                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return set_error(SP_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     }
-    kern<<<(unsigned)grid, C::NT, C::SMEM, stream>>>(p, tmap);
+    kern<<<(unsigned)grid, C::NT, C::SMEM, q.stream>>>(p, tmap);
     count_launch();
     return check_launch("k_temporal");
+}
+
+static int dispatch(int levels, const LaunchReq &q) {
+    const int idx = (int)tuning().cfg_index[levels];
+    switch (levels) {
+    case 1: return launch_cfg<1, 32, 4, 4>(q);
+    case 2:
+        switch (idx) {
+        case 1: return launch_cfg<2, 32, 4, 4>(q);
+        default: return launch_cfg<2, 32, 4, 6>(q);
+        }
+    case 3:
+        switch (idx) {
+        case 1: return launch_cfg<3, 32, 4, 3>(q);
+        default: return launch_cfg<3, 32, 4, 5>(q);
+        }
+    case 4:
+        switch (idx) {
+        case 1: return launch_cfg<4, 32, 4, 3>(q);
+        case 2: return launch_cfg<4, 32, 4, 5>(q);
+        default: return launch_cfg<4, 32, 4, 4>(q);
+        }
+    default:
+        return set_error(SP_EUNSUP, "levels %d unsupported", levels);
+    }
 }
 
 int launch_temporal(const double *src, double *dst, int64_t ex, int64_t ey, int64_t ez,
@@ -455,30 +563,29 @@ int launch_temporal(const double *src, double *dst, int64_t ex, int64_t ey, int6
                     int64_t zhi, bool copy_ring, cudaStream_t stream) {
     if (levels == 1)
         return launch_sweep1(src, dst, ex, ey, ez, nx, ny, nz, off, zlo, zhi, copy_ring, stream);
-    const int idx = (int)tuning().cfg_index[levels];
-#define SP_L(T, CY, R, S) \
-    return launch_cfg<T, CY, R, S>(src, dst, ex, ey, ez, nx, ny, nz, off, zlo, zhi, copy_ring, stream)
+    if (copy_ring) return set_error(SP_EUNSUP, "ring copy is fused only into the plain sweep");
+    LaunchReq q{src, dst, ex, ey, ez, nx, ny, nz, off, off, zlo, zhi, 0, nullptr, stream};
+    return dispatch(levels, q);
+}
+
+int64_t compressed_workspace(int64_t nx, int64_t ny, int levels) {
+    int ox, ex0, tx, ty;
     switch (levels) {
-    case 2:
-        switch (idx) {
-        case 1: SP_L(2, 32, 4, 4);
-        default: SP_L(2, 32, 4, 6);
-        }
-    case 3:
-        switch (idx) {
-        case 1: SP_L(3, 32, 4, 3);
-        default: SP_L(3, 32, 4, 5);
-        }
-    case 4:
-        switch (idx) {
-        case 1: SP_L(4, 32, 4, 3);
-        case 2: SP_L(4, 32, 4, 5);
-        default: SP_L(4, 32, 4, 4);
-        }
-    default:
-        return set_error(SP_EUNSUP, "levels %d unsupported", levels);
+    // off = levels gives par = 1: the narrower stored tile, i.e. the most tiles
+    case 1: tile_geometry<1, 32>(nx, ny, 1, true, &ox, &ex0, &tx, &ty); break;
+    case 2: tile_geometry<2, 32>(nx, ny, 2, true, &ox, &ex0, &tx, &ty); break;
+    case 3: tile_geometry<3, 32>(nx, ny, 3, true, &ox, &ex0, &tx, &ty); break;
+    default: tile_geometry<4, 32>(nx, ny, 4, true, &ox, &ex0, &tx, &ty); break;
     }
-#undef SP_L
+    return 128 + 4 * (int64_t)tx * ty;  // worst-case parity (par = 1)
+}
+
+int launch_compressed(double *data, int64_t ex, int64_t ey, int64_t ez, int64_t nx, int64_t ny,
+                      int64_t nz, int64_t src_off, int direction, int levels, int64_t zlo,
+                      int64_t zhi, void *ws, cudaStream_t stream) {
+    const int64_t doff = src_off - (direction > 0 ? levels : -levels);
+    LaunchReq q{data, data, ex, ey, ez, nx, ny, nz, src_off, doff, zlo, zhi, direction, ws, stream};
+    return dispatch(levels, q);
 }
 
 }  // namespace sp200

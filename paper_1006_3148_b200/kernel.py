@@ -146,3 +146,27 @@ def fused_sweeps(src: Grid3, dst: Grid3, levels: int, zlo: int = 0, zhi: int | N
     _lib.check(_lib.load().sp_temporal(
         _ptr(src.data), _ptr(dst.data), ex, ey, ez, src.nx, src.ny, src.nz, src.offset,
         int(levels), int(zlo), int(src.nz if zhi is None else zhi), _stream()), "fused_sweeps")
+
+
+def compressed_pass(grid: Grid3, levels: int, direction: int, src_alignment: int,
+                    workspace: torch.Tensor, zlo: int = 0, zhi: int | None = None,
+                    side_mask: int = 63) -> None:
+    """K3: `levels` (1..4) in-place shifted updates of a compressed grid in one
+    HBM pass, frame a -> a +/- levels (sp/pipeline.py:309-312), then the
+    Dirichlet faces at the new frame (sp/kernel.py:61-82)."""
+    ex, ey, ez = grid.extents
+    faces = grid.face_pointers()
+    mask = 0
+    for n, key in enumerate(FACE_KEYS):
+        if (side_mask >> n) & 1 and grid.boundary_faces.get(key) is not None:
+            mask |= 1 << n
+    _lib.check(_lib.load().sp_compressed(
+        _ptr(grid.data), ex, ey, ez, grid.nx, grid.ny, grid.nz, grid.origin - src_alignment,
+        int(direction), int(levels), int(zlo), int(grid.nz if zhi is None else zhi),
+        _ptr(workspace), ctypes.cast(faces, ctypes.POINTER(ctypes.c_void_p)), mask, _stream()),
+        "compressed_pass")
+
+
+def compressed_workspace(grid: Grid3, levels: int) -> torch.Tensor:
+    n = int(_lib.load().sp_compressed_workspace(grid.nx, grid.ny, grid.nz, int(levels)))
+    return torch.empty(max(n, 256), dtype=torch.uint8, device=grid.data.device)

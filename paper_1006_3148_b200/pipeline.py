@@ -31,7 +31,8 @@ import torch
 
 from . import _lib
 from .grid import BlockSpec, Grid3, decompose_blocks
-from .kernel import apply_window, fused_sweeps, write_faces, write_ring_strips
+from .kernel import (apply_window, compressed_pass, compressed_workspace, fused_sweeps,
+                     write_faces, write_ring_strips)
 
 MAX_FUSED = _lib.SP_MAX_FUSED
 
@@ -333,6 +334,18 @@ class PipelineEngine:
         # _write_full_ring (sp/pipeline.py:427-447) at the pass's source frame
         write_faces(g, g.origin - a0, mask)
         lives = self._lives(h)
+        if self._fusable(lives, h):
+            # K3: fused in-place passes; each leaves the faces at its new frame
+            u0, a = 0, a0
+            launches = 1
+            for c in split_levels(h, self.max_fused):
+                ws = self._workspace(c)
+                zlo, zhi = lives[u0 + c][2]
+                compressed_pass(g, c, direction, a, ws, zlo, zhi, mask)
+                launches += 2
+                a += s * c
+                u0 += c
+            return launches
         sides = [(name, side) for ax, name in enumerate("xyz") for side in (0, 1)
                  if self.physical_sides[ax][side]]
         for u in range(1, h + 1):
@@ -341,7 +354,14 @@ class PipelineEngine:
             win = tuple(lives[u])
             apply_window(g.data, g.data, win, so, do)
             write_ring_strips(g.data, g.boundary_faces, win, do, sides, self.dims)
-        return 2 * h
+        return 2 * h + 1
+
+    def _workspace(self, levels):
+        ws = getattr(self, "_ws", {})
+        if levels not in ws:
+            ws[levels] = compressed_workspace(self.grids[0], levels)
+            self._ws = ws
+        return ws[levels]
 
     def run_pass(self, direction: int) -> RunStats:
         """One team sweep: every interior cell receives h updates

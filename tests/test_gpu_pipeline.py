@@ -209,3 +209,19 @@ def test_large_config_c3_compressed(golden):
     st = sp.run_pipelined(g, cfg, 16)
     assert st.result.alignment == 0
     assert st.result.checksum() == c["digest"]
+
+
+@pytest.mark.parametrize("dims,t,passes", [((70, 40, 30), 4, 2), ((130, 96, 24), 3, 4),
+                                           ((200, 150, 20), 2, 2), ((33, 64, 17), 1, 2),
+                                           ((300, 200, 16), 4, 2)])
+def test_compressed_fused_in_place(dims, t, passes):
+    """K3 over many tiles (ticket order + progress flags), both directions."""
+    d0 = oracle.make_storage(*dims, init="random", seed=11, ring=0.5, lo=-1.0, hi=1.0)
+    g = sp.create_grid(*dims, pad=t, init="random", seed=11, ring=0.5, lo=-1.0, hi=1.0)
+    cfg = sp.PipelineConfig(spec=sp.BlockSpec(dims[0], 4, 4), t=t, grid_mode="compressed")
+    eng = sp.PipelineEngine(cfg, g)
+    for p in range(passes):
+        eng.run_pass(1 if p % 2 == 0 else -1)
+        exp = oracle.interior(oracle.sweeps(d0, dims, t * (p + 1)), *dims)
+        assert_bitwise(g.interior_numpy(), exp)
+    assert g.alignment == 0
