@@ -326,6 +326,17 @@ def run_ours(args):
                            "frac_of_hbm_roofline": glups * (16.0 / t) / peak}
         extra["per_depth"] = per
         extra["plain_sweep_glups"] = per["1"]["glups"]
+        extra["fused_vs_plain"] = per[str(args.t)]["glups"] / per["1"]["glups"]
+        # C3: compressed single-array grid, 600^3 (pad 4), U[-1,1), 64 sweeps at
+        # t=4 through run_pipelined (K3 in-place passes), one timed solve
+        g3 = sp.create_grid(600, 600, 600, pad=4, init="random", seed=SEED, lo=-1.0, hi=1.0)
+        cfg3 = sp.PipelineConfig(spec=sp.BlockSpec(600, 30, 30), t=4, grid_mode="compressed")
+        sp.run_pipelined(g3, cfg3, 2)  # warm-up (alignment returns to 0)
+        st3 = sp.run_pipelined(g3, cfg3, 16)
+        extra["C3_compressed"] = {"glups": st3.mlups / 1e3, "sweeps": 64,
+                                  "wall_s": st3.wall_seconds,
+                                  "config": "600^3 in 606^3 (pad 4), t=4 x16 passes, in place"}
+        del g3
 
     # --- e2e through the public API with host buffers --------------------------
     e2e = None

@@ -129,17 +129,20 @@ int sp_temporal(const double *src, double *dst, int64_t ex, int64_t ey, int64_t 
  * Compressed-grid pass (K3).  Replaces `levels` update levels of
  * PipelineEngine.run_pass in compressed mode (sp/pipeline.py:309-312, 324-335,
  * 427-447): one array, level u read at frame a0 + s*(u-1) and written at frame
- * a0 + s*u (s = +1 forward / -1 backward, frame offset = pad + 1 - alignment).
- * `src_off` = pad + 1 - a0, `direction` = +1/-1.  In-place safety across CTAs
- * is enforced with device-side progress flags; `flags` is a device workspace of
- * sp_compressed_workspace() bytes (zeroed by the call).  Ring cells are read at
- * the source frame (caller writes the faces there first) and the faces are
- * written at the destination frame afterwards when faces != NULL.
+ * a0 + s*u (s = +1 forward / -1 backward; frame offset = pad + 1 - alignment),
+ * fused into one HBM pass frame a0 -> a0 + s*levels.  `src_off` = pad + 1 - a0.
+ * Ring cells are read at the source frame (the caller writes the faces there
+ * first); the faces are written at the destination frame afterwards when
+ * faces != NULL.  Outputs whose shifted store would land in another tile's
+ * read region go through `workspace` (a band stash) and are copied into place
+ * by a second kernel, so no inter-CTA ordering is needed.
+ * sp_compressed_workspace() returns the workspace bytes for a pass over
+ * `depth` = zhi - zlo planes.
  */
-int64_t sp_compressed_workspace(int64_t nx, int64_t ny, int64_t nz, int levels);
+int64_t sp_compressed_workspace(int64_t nx, int64_t ny, int64_t depth, int levels);
 int sp_compressed(double *data, int64_t ex, int64_t ey, int64_t ez,
                   int64_t nx, int64_t ny, int64_t nz, int64_t src_off, int direction,
-                  int levels, int64_t zlo, int64_t zhi, void *flags,
+                  int levels, int64_t zlo, int64_t zhi, void *workspace,
                   const double *const faces[6], int side_mask, void *stream);
 
 /* Tuning knobs (benchmarking only; results never depend on them).

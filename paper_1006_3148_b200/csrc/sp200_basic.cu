@@ -453,10 +453,9 @@ int sp_temporal(const double *src, double *dst, int64_t ex, int64_t ey, int64_t 
 
 int sp_tma_eligible(int64_t ex, int64_t ey) { return tma_eligible(nullptr, ex, ey) ? 1 : 0; }
 
-int64_t sp_compressed_workspace(int64_t nx, int64_t ny, int64_t nz, int levels) {
-    (void)nz;
-    if (nx < 1 || ny < 1 || levels < 1 || levels > SP_MAX_FUSED) return 0;
-    return compressed_workspace(nx, ny, levels);
+int64_t sp_compressed_workspace(int64_t nx, int64_t ny, int64_t depth, int levels) {
+    if (nx < 1 || ny < 1 || depth < 1 || levels < 1 || levels > SP_MAX_FUSED) return 0;
+    return compressed_workspace(nx, ny, depth, levels);
 }
 
 int sp_compressed(double *data, int64_t ex, int64_t ey, int64_t ez, int64_t nx, int64_t ny,

@@ -31,7 +31,7 @@ int launch_temporal(const double *src, double *dst, int64_t ex, int64_t ey, int6
                     int64_t nx, int64_t ny, int64_t nz, int64_t off, int levels, int64_t zlo,
                     int64_t zhi, bool copy_ring, cudaStream_t stream);
 bool tma_eligible(const void *ptr, int64_t ex, int64_t ey);
-int64_t compressed_workspace(int64_t nx, int64_t ny, int levels);
+int64_t compressed_workspace(int64_t nx, int64_t ny, int64_t depth, int levels);
 int launch_compressed(double *data, int64_t ex, int64_t ey, int64_t ez, int64_t nx, int64_t ny,
                       int64_t nz, int64_t src_off, int direction, int levels, int64_t zlo,
                       int64_t zhi, void *ws, cudaStream_t stream);

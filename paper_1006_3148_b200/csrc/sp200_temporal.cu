@@ -46,8 +46,8 @@ struct TParams {
     int zlo, zhi, zc;
     int doff;        // storage offset of logical 0 in the written frame
     int direction;   // K3: +1 forward (write shifted -T), -1 backward
-    int *ticket;     // K3: tile ticket counter
-    unsigned *prog;  // K3: per-tile progress (input planes delivered)
+    double *stash_x, *stash_y, *stash_z;  // K3 band stash
+    int wx2, hy2;    // stash_x row width, stash_y rows per plane
 };
 
 template <int T, int CY, int R, int S>
@@ -87,14 +87,14 @@ __device__ __forceinline__ void stg2_stream(double *p, double a, double b) {
 }
 
 // COMP: the compressed single-array pass (K3).  Reads the level-0 frame at
-// p.off and writes level T into the same array at p.doff = p.off -/+ T.  The
-// write of a tile lands in the read regions of its lower (forward) / upper
-// (backward) x-y neighbours, so tiles are taken in that order from a global
-// ticket counter and a tile publishes, per z step, how many input planes its
-// TMA loads have delivered; before storing plane Q a tile waits until its
-// three predecessor tiles have loaded plane Q -/+ T.  Predecessors hold
-// smaller tickets, so they are resident or done: the wait cannot deadlock.
-// This is the paper's relaxed pipeline synchronisation (Eq. 3) between CTAs.
+// p.off and writes level T into the same array at p.doff = p.off -/+ T.  A
+// tile's shifted writes overlap the read regions of its lower (forward) or
+// upper (backward) neighbours only inside a 2T-wide band along that edge (x,
+// y, and the z-chunk edge).  Band outputs go to a side buffer (the "stash")
+// and are copied into place by k_unstash after the pass; everything else is
+// written in place.  No inter-CTA ordering is needed, so K3 runs on K2's
+// tile-fastest schedule (the reference needs the same order-dependence only
+// because its blocks run in lexicographic order, sp/grid.py:195-204).
 template <int T, int CY, int R, int S, bool TMA, bool COMP>
 __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
     k_temporal(const TParams p, const __grid_constant__ CUtensorMap tmap) {
@@ -106,7 +106,6 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
     double *stage = sm;
     double *lev = sm + S * PLANE_AL;
     uint64_t *bar = reinterpret_cast<uint64_t *>(lev + C::NLEV * PLANE_AL);
-    int *tile_slot = reinterpret_cast<int *>(bar + S);
 
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
@@ -137,30 +136,14 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
 
     uint32_t gbase = 0;  // stage loads issued by this CTA before the current unit
     for (int unit = 0;; ++unit) {
-    int tile, z0, z1;
-    if constexpr (COMP) {
-        // persistent CTAs, tickets in predecessor-first order
-        if (tid == 0) {
-            const int t = atomicAdd(p.ticket, 1);
-            *tile_slot = t;
-        }
-        __syncthreads();
-        const int t = *tile_slot;
-        __syncthreads();
-        if (t >= p.ntiles) break;
-        tile = (p.direction > 0) ? t : p.ntiles - 1 - t;
-        z0 = p.zlo;
-        z1 = p.zhi;
-    } else {
-        if (unit > 0) break;
-        // one (tile, z-chunk) unit per CTA, tile-fastest so that concurrently
-        // running CTAs cover neighbouring tiles at the same z range and the
-        // overlapped halo reads hit L2
-        tile = blockIdx.x % p.ntiles;
-        const int chunk = blockIdx.x / p.ntiles;
-        z0 = p.zlo + chunk * p.zc;
-        z1 = min(z0 + p.zc, p.zhi);
-    }
+    if (unit > 0) break;
+    // one (tile, z-chunk) unit per CTA, tile-fastest so that concurrently
+    // running CTAs cover neighbouring tiles at the same z range and the
+    // overlapped halo reads hit L2
+    const int tile = blockIdx.x % p.ntiles;
+    const int chunk = blockIdx.x / p.ntiles;
+    const int z0 = p.zlo + chunk * p.zc;
+    const int z1 = min(z0 + p.zc, p.zhi);
     const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
     const int x0 = tx * p.ox, y0 = ty * C::OY;
     const int rx0 = x0 - p.ex0, ry0 = y0 - (T - 1);  // logical coords of region (0, 0)
@@ -193,11 +176,28 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
     const int64_t pz = p.ex * p.ey;
     double *dcol = p.dst + (int64_t)(ry0 + j0 + p.doff) * p.ex + (rx0 + i0 + p.doff);
 
-    // K3 predecessor tiles (forward: x-1, y-1, both; backward: x+1, y+1, both)
-    const int dxn = (p.direction > 0) ? -1 : 1;
-    const bool hx = COMP && (tx + dxn >= 0) && (tx + dxn < p.tiles_x);
-    const bool hy = COMP && (ty + dxn >= 0) && (ty + dxn < p.tiles_y);
-    const int tpx = tile + dxn, tpy = tile + dxn * p.tiles_x, tpxy = tile + dxn * (p.tiles_x + 1);
+    // K3 bands: outputs whose shifted store would land in a neighbour's read
+    // region go to the stash (forward: the low 2T columns / rows / planes of
+    // the tile unless it is the first; backward: the high 2T unless last)
+    const bool fwd = p.direction > 0;
+    bool xb[2];
+    int kx[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const int xo = rx0 + i0 + c - x0;  // column within the stored tile
+        xb[c] = COMP && (fwd ? (tx > 0 && xo < 2 * T) : (tx < p.tiles_x - 1 && xo >= p.ox - 2 * T));
+        kx[c] = fwd ? (tx - 1) * 2 * T + xo : tx * 2 * T + xo - (p.ox - 2 * T);
+    }
+    bool yb[R];
+    int ky[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int yo = ry0 + j0 + r - y0;
+        yb[r] = COMP && (fwd ? (ty > 0 && yo < 2 * T) : (ty < p.tiles_y - 1 && yo >= C::OY - 2 * T));
+        ky[r] = fwd ? (ty - 1) * 2 * T + yo : ty * 2 * T + yo - (C::OY - 2 * T);
+    }
+    const int nchunks = (p.zhi - p.zlo + p.zc - 1) / p.zc;
+    const bool zband_chunk = COMP && (fwd ? chunk > 0 : chunk < nchunks - 1);
 
     auto issue = [&](int s) {
         const int si = (int)((gbase + s) % S);
@@ -316,8 +316,27 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
                     if (r == 0 || r == R - 1) sts2(pub + (j0 + r + 1) * SPX + C0 + i0, v[r][0], v[r][1]);
                 } else if (store_plane && y_out[r]) {
                     double *g = dcol + (int64_t)(pout + p.doff) * pz + (int64_t)r * p.ex;
-                    if (x_out[0] && x_out[1] && p.pair_store) stg2_stream(g, v[r][0], v[r][1]);
-                    else {
+                    if constexpr (COMP) {
+                        const int zo = pout - z0;
+                        const bool zb = zband_chunk && (fwd ? zo < 2 * T : zo >= (z1 - z0) - 2 * T);
+                        const int kz = fwd ? (chunk - 1) * 2 * T + zo : chunk * 2 * T + zo - ((z1 - z0) - 2 * T);
+                        const int y = ry0 + j0 + r;
+#pragma unroll
+                        for (int c = 0; c < 2; ++c) {
+                            if (!x_out[c]) continue;
+                            const int x = rx0 + i0 + c;
+                            if (xb[c])
+                                p.stash_x[((int64_t)(pout - p.zlo) * p.ny + y) * p.wx2 + kx[c]] = v[r][c];
+                            else if (yb[r])
+                                p.stash_y[((int64_t)(pout - p.zlo) * p.hy2 + ky[r]) * p.nx + x] = v[r][c];
+                            else if (zb)
+                                p.stash_z[((int64_t)kz * p.ny + y) * p.nx + x] = v[r][c];
+                            else
+                                st_stream(g + c, v[r][c]);
+                        }
+                    } else if (x_out[0] && x_out[1] && p.pair_store) {
+                        stg2_stream(g, v[r][0], v[r][1]);
+                    } else {
                         if (x_out[0]) st_stream(g, v[r][0]);
                         if (x_out[1]) st_stream(g + 1, v[r][1]);
                     }
@@ -332,22 +351,6 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
             if (s < nload) mbar_wait(&bar[si], (uint32_t)(((gbase + s) / S) & 1));
         } else {
             cp_async_wait<S - 2>();
-        }
-        if constexpr (COMP) {
-            if (tid == 0) {
-                // publish: input planes of this tile delivered so far
-                st_release_gpu(p.prog + tile, (unsigned)(s + 1));
-                // before this step stores plane Q = z0+s-3T+1 (frame shift
-                // -/+T), the predecessors must have loaded input plane Q -/+ T,
-                // i.e. completed their step s-3T+1 (and, for the backward pass,
-                // 2T further)
-                const int need = s - 3 * T + 2 + ((p.direction > 0) ? 0 : 2 * T);
-                if (need > 0) {
-                    if (hx) while ((int)ld_acquire_gpu(p.prog + tpx) < need) __nanosleep(64);
-                    if (hy) while ((int)ld_acquire_gpu(p.prog + tpy) < need) __nanosleep(64);
-                    if (hx && hy) while ((int)ld_acquire_gpu(p.prog + tpxy) < need) __nanosleep(64);
-                }
-            }
         }
         __syncthreads();
         if constexpr (TMA) {
@@ -370,12 +373,69 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
         if (s + 1 < nsteps) one_step(s + 1, IC<1>{});
     }
     if constexpr (!TMA) cp_async_wait<0>();
-    if constexpr (COMP) {
-        __syncthreads();
-        if (tid == 0) st_release_gpu(p.prog + tile, 0x7fffffffu);  // tile done
-    }
     gbase += (uint32_t)nload;
     }  // units
+}
+
+struct UnstashArgs {
+    double *data;
+    int64_t ex, ey;
+    int nx, ny, doff, zlo, zhi, zc, nchunks, ox, oy, tiles_x, tiles_y, T2, fwd;
+    const double *sx, *sy, *sz;
+    int wx2, hy2;
+};
+
+// K3 epilogue: copy the stashed band outputs to their shifted frame.  The
+// three stashes hold disjoint cell sets (x band first, then y, then z).
+__global__ void k_unstash(UnstashArgs a) {
+    const int64_t nxs = (int64_t)(a.zhi - a.zlo) * a.ny * a.wx2;
+    const int64_t nys = (int64_t)(a.zhi - a.zlo) * a.hy2 * a.nx;
+    const int64_t nzs = (int64_t)(a.nchunks - 1) * a.T2 * a.ny * a.nx;
+    const int64_t total = nxs + nys + nzs;
+    auto in_xband = [&](int x) {
+        const int tx = x / a.ox, xo = x - tx * a.ox;
+        return a.fwd ? (tx > 0 && xo < a.T2) : (tx < a.tiles_x - 1 && xo >= a.ox - a.T2);
+    };
+    auto in_yband = [&](int y) {
+        const int ty = y / a.oy, yo = y - ty * a.oy;
+        return a.fwd ? (ty > 0 && yo < a.T2) : (ty < a.tiles_y - 1 && yo >= a.oy - a.T2);
+    };
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        int x, y, z;
+        double v;
+        if (idx < nxs) {
+            const int k = (int)(idx % a.wx2);
+            const int64_t r = idx / a.wx2;
+            y = (int)(r % a.ny);
+            z = a.zlo + (int)(r / a.ny);
+            const int bt = k / a.T2, bo = k % a.T2;
+            x = a.fwd ? (bt + 1) * a.ox + bo : bt * a.ox + a.ox - a.T2 + bo;
+            if (x >= a.nx) continue;
+            v = a.sx[((int64_t)(z - a.zlo) * a.ny + y) * a.wx2 + k];
+        } else if (idx < nxs + nys) {
+            const int64_t q = idx - nxs;
+            x = (int)(q % a.nx);
+            const int64_t r = q / a.nx;
+            const int k = (int)(r % a.hy2);
+            z = a.zlo + (int)(r / a.hy2);
+            const int bt = k / a.T2, bo = k % a.T2;
+            y = a.fwd ? (bt + 1) * a.oy + bo : bt * a.oy + a.oy - a.T2 + bo;
+            if (y >= a.ny || in_xband(x)) continue;
+            v = a.sy[((int64_t)(z - a.zlo) * a.hy2 + k) * a.nx + x];
+        } else {
+            const int64_t q = idx - nxs - nys;
+            x = (int)(q % a.nx);
+            const int64_t r = q / a.nx;
+            y = (int)(r % a.ny);
+            const int k = (int)(r / a.ny);
+            const int bt = k / a.T2, bo = k % a.T2;
+            z = a.zlo + (a.fwd ? (bt + 1) * a.zc + bo : bt * a.zc + a.zc - a.T2 + bo);
+            if (z >= a.zhi || in_xband(x) || in_yband(y)) continue;
+            v = a.sz[((int64_t)k * a.ny + y) * a.nx + x];
+        }
+        a.data[((int64_t)(z + a.doff) * a.ey + (y + a.doff)) * a.ex + (x + a.doff)] = v;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -414,7 +474,7 @@ struct LaunchReq {
     double *dst;
     int64_t ex, ey, ez, nx, ny, nz, off, doff, zlo, zhi;
     int direction;  // 0: two-grid (K1/K2); +1/-1: compressed in place (K3)
-    void *ws;       // K3 workspace (ticket + per-tile progress)
+    void *ws;       // K3 workspace: the band stash
     cudaStream_t stream;
 };
 
@@ -428,6 +488,48 @@ static int tile_geometry(int64_t nx, int64_t ny, int64_t off, bool aligned, int 
     *tiles_x = (int)((nx + *ox - 1) / *ox);
     *tiles_y = (int)((ny + C::OY - 1) / C::OY);
     return par;
+}
+
+static int64_t pick_zchunk(int64_t depth, int64_t ntiles, int64_t slots, int T) {
+    double best = 1e300;
+    int64_t zc = depth;
+    for (int64_t c = 1; c <= 256 && c <= depth; ++c) {
+        int64_t len = (depth + c - 1) / c;
+        int64_t units = ntiles * ((depth + len - 1) / len);
+        double waves = (double)((units + slots - 1) / slots);
+        // a partial last wave still costs a whole wave; a short chunk pays the
+        // (3T-1)-step pipeline fill/drain
+        double cost = waves * (double)(len + 3 * T - 1);
+        if (cost < best * 0.999) {
+            best = cost;
+            zc = len;
+        }
+    }
+    return zc;
+}
+
+struct CompLayout {
+    int64_t zc, nchunks, nx_stash, ny_stash, nz_stash;
+    int wx2, hy2;
+};
+
+// K3 geometry: z-chunks (>= 2T planes, one CTA per SM assumed so the layout is
+// the same for sizing and launch) and the three band stashes.
+template <int T, int CY>
+static void comp_layout(int64_t nx, int64_t ny, int64_t depth, int64_t off, bool aligned,
+                        CompLayout *L) {
+    int ox, ex0, tx, ty;
+    tile_geometry<T, CY>(nx, ny, off, aligned, &ox, &ex0, &tx, &ty);
+    int64_t zc = tuning().zchunk > 0 ? tuning().zchunk
+                                     : pick_zchunk(depth, (int64_t)tx * ty, sm_count(), T);
+    if (zc < 2 * T) zc = std::min<int64_t>(depth, 2 * T);
+    L->zc = zc;
+    L->nchunks = (depth + zc - 1) / zc;
+    L->wx2 = (tx - 1) * 2 * T;
+    L->hy2 = (ty - 1) * 2 * T;
+    L->nx_stash = depth * ny * L->wx2;
+    L->ny_stash = depth * L->hy2 * nx;
+    L->nz_stash = (L->nchunks - 1) * 2 * T * ny * nx;
 }
 
 template <int T, int CY, int R, int S>
@@ -463,8 +565,8 @@ static int launch_cfg(const LaunchReq &q) {
     p.ntiles = p.tiles_x * tiles_y;
     p.zlo = (int)q.zlo;
     p.zhi = (int)q.zhi;
-    p.ticket = nullptr;
-    p.prog = nullptr;
+    p.stash_x = p.stash_y = p.stash_z = nullptr;
+    p.wx2 = p.hy2 = 0;
 
     void (*kern)(const TParams, const CUtensorMap);
     if (comp)
@@ -482,33 +584,21 @@ static int launch_cfg(const LaunchReq &q) {
     if (occ < 1) occ = 1;
     const int64_t slots = (int64_t)sm_count() * occ;
     int64_t grid;
+    CompLayout L;
     if (comp) {
-        // persistent CTAs walking full columns in ticket order
-        p.zc = (int)depth;
-        grid = std::min<int64_t>(slots, p.ntiles);
-        p.ticket = reinterpret_cast<int *>(q.ws);
-        p.prog = reinterpret_cast<unsigned *>(reinterpret_cast<char *>(q.ws) + 128);
-        e = cudaMemsetAsync(q.ws, 0, 128 + (size_t)p.ntiles * 4, q.stream);
-        if (e != cudaSuccess)
-            return set_error(SP_ECUDA, "cudaMemsetAsync: %s", cudaGetErrorString(e));
+        comp_layout<T, CY>(q.nx, q.ny, q.zhi - q.zlo, q.off, aligned, &L);
+        p.zc = (int)L.zc;
+        grid = (int64_t)p.ntiles * L.nchunks;
+        char *ws = reinterpret_cast<char *>(q.ws);
+        p.stash_x = reinterpret_cast<double *>(ws);
+        p.stash_y = p.stash_x + L.nx_stash;
+        p.stash_z = p.stash_y + L.ny_stash;
+        p.wx2 = L.wx2;
+        p.hy2 = L.hy2;
     } else {
         // z-chunking: choose the chunk count minimising (waves x steps per chunk)
         int64_t zc = tuning().zchunk;
-        if (zc <= 0) {
-            double best = 1e300;
-            for (int64_t c = 1; c <= 256 && c <= depth; ++c) {
-                int64_t len = (depth + c - 1) / c;
-                int64_t units = p.ntiles * ((depth + len - 1) / len);
-                double waves = (double)((units + slots - 1) / slots);
-                // a partial last wave still costs a whole wave; a short chunk
-                // pays the (3T-1)-step pipeline fill/drain
-                double cost = waves * (double)(len + 3 * T - 1);
-                if (cost < best * 0.999) {
-                    best = cost;
-                    zc = len;
-                }
-            }
-        }
+        if (zc <= 0) zc = pick_zchunk(depth, p.ntiles, slots, T);
         if (zc < 1) zc = 1;
         p.zc = (int)zc;
         grid = (int64_t)p.ntiles * ((depth + zc - 1) / zc);
@@ -530,7 +620,38 @@ static int launch_cfg(const LaunchReq &q) {
     }
     kern<<<(unsigned)grid, C::NT, C::SMEM, q.stream>>>(p, tmap);
     count_launch();
-    return check_launch("k_temporal");
+    int rc = check_launch("k_temporal");
+    if (rc || !comp) return rc;
+    UnstashArgs u;
+    u.data = q.dst;
+    u.ex = q.ex;
+    u.ey = q.ey;
+    u.nx = (int)q.nx;
+    u.ny = (int)q.ny;
+    u.doff = (int)q.doff;
+    u.zlo = (int)q.zlo;
+    u.zhi = (int)q.zhi;
+    u.zc = (int)L.zc;
+    u.nchunks = (int)L.nchunks;
+    u.ox = p.ox;
+    u.oy = C::OY;
+    u.tiles_x = p.tiles_x;
+    u.tiles_y = p.tiles_y;
+    u.T2 = 2 * T;
+    u.fwd = q.direction > 0 ? 1 : 0;
+    u.sx = p.stash_x;
+    u.sy = p.stash_y;
+    u.sz = p.stash_z;
+    u.wx2 = p.wx2;
+    u.hy2 = p.hy2;
+    const int64_t total = L.nx_stash + L.ny_stash + L.nz_stash;
+    if (total > 0) {
+        int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 16);
+        k_unstash<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, q.stream>>>(u);
+        count_launch();
+        rc = check_launch("k_unstash");
+    }
+    return rc;
 }
 
 static int dispatch(int levels, const LaunchReq &q) {
@@ -568,16 +689,16 @@ int launch_temporal(const double *src, double *dst, int64_t ex, int64_t ey, int6
     return dispatch(levels, q);
 }
 
-int64_t compressed_workspace(int64_t nx, int64_t ny, int levels) {
-    int ox, ex0, tx, ty;
+int64_t compressed_workspace(int64_t nx, int64_t ny, int64_t depth, int levels) {
+    CompLayout L;
+    // off = levels gives par = 1: the narrower stored tile, i.e. the most bands
     switch (levels) {
-    // off = levels gives par = 1: the narrower stored tile, i.e. the most tiles
-    case 1: tile_geometry<1, 32>(nx, ny, 1, true, &ox, &ex0, &tx, &ty); break;
-    case 2: tile_geometry<2, 32>(nx, ny, 2, true, &ox, &ex0, &tx, &ty); break;
-    case 3: tile_geometry<3, 32>(nx, ny, 3, true, &ox, &ex0, &tx, &ty); break;
-    default: tile_geometry<4, 32>(nx, ny, 4, true, &ox, &ex0, &tx, &ty); break;
+    case 1: comp_layout<1, 32>(nx, ny, depth, 1, true, &L); break;
+    case 2: comp_layout<2, 32>(nx, ny, depth, 2, true, &L); break;
+    case 3: comp_layout<3, 32>(nx, ny, depth, 3, true, &L); break;
+    default: comp_layout<4, 32>(nx, ny, depth, 4, true, &L); break;
     }
-    return 128 + 4 * (int64_t)tx * ty;  // worst-case parity (par = 1)
+    return 8 * (L.nx_stash + L.ny_stash + L.nz_stash) + 256;
 }
 
 int launch_compressed(double *data, int64_t ex, int64_t ey, int64_t ez, int64_t nx, int64_t ny,

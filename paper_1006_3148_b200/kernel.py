@@ -167,6 +167,8 @@ def compressed_pass(grid: Grid3, levels: int, direction: int, src_alignment: int
         "compressed_pass")
 
 
-def compressed_workspace(grid: Grid3, levels: int) -> torch.Tensor:
-    n = int(_lib.load().sp_compressed_workspace(grid.nx, grid.ny, grid.nz, int(levels)))
+def compressed_workspace(grid: Grid3, levels: int, depth: int | None = None) -> torch.Tensor:
+    """Band-stash workspace for a K3 pass over `depth` planes (default nz)."""
+    n = int(_lib.load().sp_compressed_workspace(grid.nx, grid.ny, grid.nz if depth is None else depth,
+                                                int(levels)))
     return torch.empty(max(n, 256), dtype=torch.uint8, device=grid.data.device)

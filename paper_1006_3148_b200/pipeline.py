@@ -339,8 +339,8 @@ class PipelineEngine:
             u0, a = 0, a0
             launches = 1
             for c in split_levels(h, self.max_fused):
-                ws = self._workspace(c)
                 zlo, zhi = lives[u0 + c][2]
+                ws = self._workspace(c, zhi - zlo)
                 compressed_pass(g, c, direction, a, ws, zlo, zhi, mask)
                 launches += 2
                 a += s * c
@@ -356,12 +356,12 @@ class PipelineEngine:
             write_ring_strips(g.data, g.boundary_faces, win, do, sides, self.dims)
         return 2 * h + 1
 
-    def _workspace(self, levels):
+    def _workspace(self, levels, depth):
         ws = getattr(self, "_ws", {})
-        if levels not in ws:
-            ws[levels] = compressed_workspace(self.grids[0], levels)
+        if (levels, depth) not in ws:
+            ws[(levels, depth)] = compressed_workspace(self.grids[0], levels, depth)
             self._ws = ws
-        return ws[levels]
+        return ws[(levels, depth)]
 
     def run_pass(self, direction: int) -> RunStats:
         """One team sweep: every interior cell receives h updates
