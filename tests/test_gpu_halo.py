@@ -73,3 +73,20 @@ def test_golden_distributed_digests(golden):
         dc = halo.DistConfig(topo=halo.RankTopology(*c["topo"]), cfg=cfg, cycles=c["cycles"],
                              global_dims=tuple(c["global_dims"]), mode="strong", seed=c["seed"])
         assert _emulate(dc).checksum() == c["digest"], name
+
+
+@pytest.mark.slow
+def test_c4_weak_scaling_p2_window_oracle():
+    """BASELINE configs[3] at P=2 (1024^2 x 2048, ring 1.0, t=4, 40 sweeps),
+    every rank on this GPU; boxes straddling the rank boundary and touching
+    the physical faces checked with the light-cone window oracle."""
+    cfg = sp.PipelineConfig(spec=sp.BlockSpec(64, 32, 32), t=4)
+    dc = halo.DistConfig(topo=halo.RankTopology(1, 1, 2), cfg=cfg, cycles=10,
+                         per_rank_dims=(1024, 1024, 1024), mode="weak", seed=42, ring=1.0)
+    g = _emulate(dc)
+    gd = dc.resolved_global()
+    for box in (((0, 48), (480, 528), (1016, 1032)), ((990, 1024), (0, 40), (2040, 2048)),
+                ((500, 540), (1000, 1024), (0, 12))):
+        exp = oracle.window_oracle(gd, 42, box, 40, ring=1.0)
+        (xl, xh), (yl, yh), (zl, zh) = box
+        assert_bitwise(g.interior_view()[zl:zh, yl:yh, xl:xh].cpu().numpy(), exp)

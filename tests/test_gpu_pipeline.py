@@ -225,3 +225,15 @@ def test_compressed_fused_in_place(dims, t, passes):
         exp = oracle.interior(oracle.sweeps(d0, dims, t * (p + 1)), *dims)
         assert_bitwise(g.interior_numpy(), exp)
     assert g.alignment == 0
+
+
+@pytest.mark.slow
+def test_large_config_c4_single_gpu(golden):
+    """BASELINE configs[3] at P=1: 1024^3, ring 1.0, 40 sweeps (t=4 x10) —
+    digest produced by the reference's own run_pipelined."""
+    c = golden["configs"]["C4_P1"]
+    a = sp.create_grid(*c["n"], init="random", seed=c["seed"], ring=c["ring"])
+    assert a.checksum() == c["init_digest"]
+    cfg = sp.PipelineConfig(spec=sp.BlockSpec(1024, 32, 32), t=4)
+    st = sp.run_pipelined((a, a.copy()), cfg, 10)
+    assert st.result.checksum() == c["digest"]
