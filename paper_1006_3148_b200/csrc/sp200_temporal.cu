@@ -48,6 +48,7 @@ struct TParams {
     int direction;   // K3: +1 forward (write shifted -T), -1 backward
     double *stash_x, *stash_y, *stash_z;  // K3 band stash
     int wx2, hy2;    // stash_x row width, stash_y rows per plane
+    int debug;       // profiling only (sp_set_tuning key 4): 1 skip levels, 2 skip loads, 4 skip barrier
 };
 
 template <int T, int CY, int R, int S>
@@ -62,6 +63,9 @@ struct KCfg {
     static constexpr int OY = CY - 2 * (T - 1);
     static constexpr int NLEV = (T > 1) ? 2 * (T - 1) : 0;
     static constexpr size_t SMEM = (size_t)(S + NLEV) * PLANE_AL * sizeof(double) + 8 * S + 16;
+    // CTAs per SM the shared memory allows (1 KB per CTA is reserved by the
+    // runtime); the register budget follows through __launch_bounds__
+    static constexpr int MINB = (2 * (SMEM + 1024) <= 232448) ? 2 : 1;
     static_assert(CY % R == 0, "rows per thread must divide CY");
     static_assert(OY > 0, "tile too small for the fused depth");
 };
@@ -96,7 +100,7 @@ __device__ __forceinline__ void stg2_stream(double *p, double a, double b) {
 // tile-fastest schedule (the reference needs the same order-dependence only
 // because its blocks run in lexicographic order, sp/grid.py:195-204).
 template <int T, int CY, int R, int S, bool TMA, bool COMP>
-__global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
+__global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB)
     k_temporal(const TParams p, const __grid_constant__ CUtensorMap tmap) {
     using C = KCfg<T, CY, R, S>;
     constexpr int SPX = C::SPX, C0 = C::C0, PLANE = C::PLANE, PLANE_AL = C::PLANE_AL,
@@ -198,6 +202,17 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
     }
     const int nchunks = (p.zhi - p.zlo + p.zc - 1) / p.zc;
     const bool zband_chunk = COMP && (fwd ? chunk > 0 : chunk < nchunks - 1);
+    // stash addressing, affine in the output plane: stash_y / stash_z rows are
+    // padded by one column so that column pairs stay 16-byte aligned
+    const int sxpad = p.ex0 & 1;
+    const int srow = (p.nx + 2) & ~1;  // even: pairs stay 16-byte aligned
+    double *sx_col[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+        sx_col[c] = COMP ? p.stash_x + ((int64_t)(ry0 + j0 - p.zlo * p.ny)) * p.wx2 + kx[c] : nullptr;
+    double *sy_col = COMP ? p.stash_y + ((int64_t)ky[0] - (int64_t)p.zlo * p.hy2) * srow + rx0 + i0 + sxpad
+                          : nullptr;
+    double *sz_col = COMP ? p.stash_z + (int64_t)(ry0 + j0) * srow + rx0 + i0 + sxpad : nullptr;
 
     auto issue = [&](int s) {
         const int si = (int)((gbase + s) % S);
@@ -219,7 +234,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
     };
 
     if constexpr (TMA) {
-        if (tid == 0)
+        if (tid == 0 && !(p.debug & 2))
             for (int s = 0; s < S - 1; ++s)
                 if (s < nload) issue(s);
     } else {
@@ -317,22 +332,35 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
                 } else if (store_plane && y_out[r]) {
                     double *g = dcol + (int64_t)(pout + p.doff) * pz + (int64_t)r * p.ex;
                     if constexpr (COMP) {
+                        // band priority y, then z, then x (k_unstash_* skip
+                        // in the same order); y and z bands are whole rows
                         const int zo = pout - z0;
                         const bool zb = zband_chunk && (fwd ? zo < 2 * T : zo >= (z1 - z0) - 2 * T);
-                        const int kz = fwd ? (chunk - 1) * 2 * T + zo : chunk * 2 * T + zo - ((z1 - z0) - 2 * T);
-                        const int y = ry0 + j0 + r;
+                        double *row = nullptr;
+                        if (yb[r]) {
+                            row = sy_col + ((int64_t)pout * p.hy2 + r) * srow;
+                        } else if (zb) {
+                            const int kz = fwd ? (chunk - 1) * 2 * T + zo
+                                               : chunk * 2 * T + zo - ((z1 - z0) - 2 * T);
+                            row = sz_col + ((int64_t)kz * p.ny + r) * srow;
+                        }
+                        if (row) {
+                            if (x_out[0] && x_out[1]) stg2_stream(row, v[r][0], v[r][1]);
+                            else {
+                                if (x_out[0]) row[0] = v[r][0];
+                                if (x_out[1]) row[1] = v[r][1];
+                            }
+                        } else if (!xb[0] && !xb[1] && x_out[0] && x_out[1] && p.pair_store) {
+                            stg2_stream(g, v[r][0], v[r][1]);
+                        } else {
 #pragma unroll
-                        for (int c = 0; c < 2; ++c) {
-                            if (!x_out[c]) continue;
-                            const int x = rx0 + i0 + c;
-                            if (xb[c])
-                                p.stash_x[((int64_t)(pout - p.zlo) * p.ny + y) * p.wx2 + kx[c]] = v[r][c];
-                            else if (yb[r])
-                                p.stash_y[((int64_t)(pout - p.zlo) * p.hy2 + ky[r]) * p.nx + x] = v[r][c];
-                            else if (zb)
-                                p.stash_z[((int64_t)kz * p.ny + y) * p.nx + x] = v[r][c];
-                            else
-                                st_stream(g + c, v[r][c]);
+                            for (int c = 0; c < 2; ++c) {
+                                if (!x_out[c]) continue;
+                                if (xb[c])
+                                    sx_col[c][((int64_t)pout * p.ny + r) * p.wx2] = v[r][c];
+                                else
+                                    st_stream(g + c, v[r][c]);
+                            }
                         }
                     } else if (x_out[0] && x_out[1] && p.pair_store) {
                         stg2_stream(g, v[r][0], v[r][1]);
@@ -348,13 +376,13 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
     auto one_step = [&](int s, auto Qc) {
         const int si = (int)((gbase + s) % S);
         if constexpr (TMA) {
-            if (s < nload) mbar_wait(&bar[si], (uint32_t)(((gbase + s) / S) & 1));
+            if (s < nload && !(p.debug & 2)) mbar_wait(&bar[si], (uint32_t)(((gbase + s) / S) & 1));
         } else {
             cp_async_wait<S - 2>();
         }
-        __syncthreads();
+        if (!(p.debug & 4)) __syncthreads();
         if constexpr (TMA) {
-            if (tid == 0 && s + S - 1 < nload) issue(s + S - 1);
+            if (tid == 0 && s + S - 1 < nload && !(p.debug & 2)) issue(s + S - 1);
         } else {
             if (s + S - 1 < nload) issue(s + S - 1);
             else cp_async_commit();
@@ -363,6 +391,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
         // every level's finished plane inside [0, nz): no z-ring this step
         const int pmax = z0 - T + s - 1, pmin = z0 - T + s - 2 * T + 1;
         const bool zall = (pmin >= 0) && (pmax < p.nz);
+        if (p.debug & 1) return;  // profiling only: skip the level updates
         if (wint && zall) levels(s, cur, Qc, IC<0>{});
         else if (zall) levels(s, cur, Qc, IC<1>{});
         else levels(s, cur, Qc, IC<2>{});
@@ -380,61 +409,54 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, 1)
 struct UnstashArgs {
     double *data;
     int64_t ex, ey;
-    int nx, ny, doff, zlo, zhi, zc, nchunks, ox, oy, tiles_x, tiles_y, T2, fwd;
+    int nx, ny, doff, zlo, zhi, zc, nchunks, ox, oy, tiles_x, tiles_y, T2, fwd, sxpad;
     const double *sx, *sy, *sz;
     int wx2, hy2;
 };
 
-// K3 epilogue: copy the stashed band outputs to their shifted frame.  The
-// three stashes hold disjoint cell sets (x band first, then y, then z).
-__global__ void k_unstash(UnstashArgs a) {
-    const int64_t nxs = (int64_t)(a.zhi - a.zlo) * a.ny * a.wx2;
-    const int64_t nys = (int64_t)(a.zhi - a.zlo) * a.hy2 * a.nx;
-    const int64_t nzs = (int64_t)(a.nchunks - 1) * a.T2 * a.ny * a.nx;
-    const int64_t total = nxs + nys + nzs;
-    auto in_xband = [&](int x) {
-        const int tx = x / a.ox, xo = x - tx * a.ox;
-        return a.fwd ? (tx > 0 && xo < a.T2) : (tx < a.tiles_x - 1 && xo >= a.ox - a.T2);
-    };
-    auto in_yband = [&](int y) {
-        const int ty = y / a.oy, yo = y - ty * a.oy;
-        return a.fwd ? (ty > 0 && yo < a.T2) : (ty < a.tiles_y - 1 && yo >= a.oy - a.T2);
-    };
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        int x, y, z;
-        double v;
-        if (idx < nxs) {
-            const int k = (int)(idx % a.wx2);
-            const int64_t r = idx / a.wx2;
-            y = (int)(r % a.ny);
-            z = a.zlo + (int)(r / a.ny);
-            const int bt = k / a.T2, bo = k % a.T2;
-            x = a.fwd ? (bt + 1) * a.ox + bo : bt * a.ox + a.ox - a.T2 + bo;
-            if (x >= a.nx) continue;
-            v = a.sx[((int64_t)(z - a.zlo) * a.ny + y) * a.wx2 + k];
-        } else if (idx < nxs + nys) {
-            const int64_t q = idx - nxs;
-            x = (int)(q % a.nx);
-            const int64_t r = q / a.nx;
-            const int k = (int)(r % a.hy2);
-            z = a.zlo + (int)(r / a.hy2);
-            const int bt = k / a.T2, bo = k % a.T2;
-            y = a.fwd ? (bt + 1) * a.oy + bo : bt * a.oy + a.oy - a.T2 + bo;
-            if (y >= a.ny || in_xband(x)) continue;
-            v = a.sy[((int64_t)(z - a.zlo) * a.hy2 + k) * a.nx + x];
-        } else {
-            const int64_t q = idx - nxs - nys;
-            x = (int)(q % a.nx);
-            const int64_t r = q / a.nx;
-            y = (int)(r % a.ny);
-            const int k = (int)(r / a.ny);
-            const int bt = k / a.T2, bo = k % a.T2;
-            z = a.zlo + (a.fwd ? (bt + 1) * a.zc + bo : bt * a.zc + a.zc - a.T2 + bo);
-            if (z >= a.zhi || in_xband(x) || in_yband(y)) continue;
-            v = a.sz[((int64_t)k * a.ny + y) * a.nx + x];
-        }
-        a.data[((int64_t)(z + a.doff) * a.ey + (y + a.doff)) * a.ex + (x + a.doff)] = v;
+__device__ __forceinline__ bool band_hit(int v, int tile, int ntiles, int o, int T2, int fwd) {
+    return fwd ? (tile > 0 && v < T2) : (tile < ntiles - 1 && v >= o - T2);
+}
+__device__ __forceinline__ int band_pos(int k, int o, int T2, int fwd) {
+    const int bt = k / T2, bo = k - bt * T2;
+    return fwd ? (bt + 1) * o + bo : bt * o + o - T2 + bo;
+}
+
+// K3 epilogue: copy the stashed band outputs to their shifted frame, one CTA
+// per stash row (no 64-bit divisions).  The three stashes hold disjoint cell
+// sets: y band first, then z band, then x band (the order K3 stores them).
+__global__ void k_unstash_y(UnstashArgs a) {
+    const int k = blockIdx.x % a.hy2, zr = blockIdx.x / a.hy2;
+    const int y = band_pos(k, a.oy, a.T2, a.fwd), z = a.zlo + zr;
+    if (y >= a.ny) return;
+    const double *src = a.sy + (int64_t)blockIdx.x * ((a.nx + 2) & ~1) + a.sxpad;
+    double *dst = a.data + ((int64_t)(z + a.doff) * a.ey + (y + a.doff)) * a.ex + a.doff;
+    for (int x = threadIdx.x; x < a.nx; x += blockDim.x) dst[x] = src[x];
+}
+
+__global__ void k_unstash_z(UnstashArgs a) {
+    const int y = blockIdx.x % a.ny, k = blockIdx.x / a.ny;
+    const int z = a.zlo + band_pos(k, a.zc, a.T2, a.fwd);
+    const int ty = y / a.oy;
+    if (z >= a.zhi || band_hit(y - ty * a.oy, ty, a.tiles_y, a.oy, a.T2, a.fwd)) return;
+    const double *src = a.sz + (int64_t)blockIdx.x * ((a.nx + 2) & ~1) + a.sxpad;
+    double *dst = a.data + ((int64_t)(z + a.doff) * a.ey + (y + a.doff)) * a.ex + a.doff;
+    for (int x = threadIdx.x; x < a.nx; x += blockDim.x) dst[x] = src[x];
+}
+
+__global__ void k_unstash_x(UnstashArgs a) {
+    const int y = blockIdx.x % a.ny, zr = blockIdx.x / a.ny;
+    const int z = a.zlo + zr;
+    const int ty = y / a.oy;
+    if (band_hit(y - ty * a.oy, ty, a.tiles_y, a.oy, a.T2, a.fwd)) return;
+    const int zo = zr % a.zc, chunk = zr / a.zc;
+    const int zlen = min(a.zc, a.zhi - a.zlo - chunk * a.zc);
+    if (a.fwd ? (chunk > 0 && zo < a.T2) : (chunk < a.nchunks - 1 && zo >= zlen - a.T2)) return;
+    const double *src = a.sx + (int64_t)blockIdx.x * a.wx2;
+    double *dst = a.data + ((int64_t)(z + a.doff) * a.ey + (y + a.doff)) * a.ex + a.doff;
+    for (int k = threadIdx.x; k < a.wx2; k += blockDim.x) {
+        const int x = band_pos(k, a.ox, a.T2, a.fwd);
+        if (x < a.nx) dst[x] = src[k];
     }
 }
 
@@ -528,8 +550,8 @@ static void comp_layout(int64_t nx, int64_t ny, int64_t depth, int64_t off, bool
     L->wx2 = (tx - 1) * 2 * T;
     L->hy2 = (ty - 1) * 2 * T;
     L->nx_stash = depth * ny * L->wx2;
-    L->ny_stash = depth * L->hy2 * nx;
-    L->nz_stash = (L->nchunks - 1) * 2 * T * ny * nx;
+    L->ny_stash = depth * L->hy2 * ((nx + 2) & ~1);
+    L->nz_stash = (L->nchunks - 1) * 2 * T * ny * ((nx + 2) & ~1);
 }
 
 template <int T, int CY, int R, int S>
@@ -566,6 +588,7 @@ static int launch_cfg(const LaunchReq &q) {
     p.zlo = (int)q.zlo;
     p.zhi = (int)q.zhi;
     p.stash_x = p.stash_y = p.stash_z = nullptr;
+    p.debug = (int)tuning().debug;
     p.wx2 = p.hy2 = 0;
 
     void (*kern)(const TParams, const CUtensorMap);
@@ -644,13 +667,21 @@ static int launch_cfg(const LaunchReq &q) {
     u.sz = p.stash_z;
     u.wx2 = p.wx2;
     u.hy2 = p.hy2;
-    const int64_t total = L.nx_stash + L.ny_stash + L.nz_stash;
-    if (total > 0) {
-        int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 16);
-        k_unstash<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, q.stream>>>(u);
+    u.sxpad = p.ex0 & 1;
+    const int64_t depth_ = q.zhi - q.zlo;
+    if (L.hy2 > 0) {
+        k_unstash_y<<<(unsigned)(depth_ * L.hy2), 128, 0, q.stream>>>(u);
         count_launch();
-        rc = check_launch("k_unstash");
     }
+    if (L.nchunks > 1) {
+        k_unstash_z<<<(unsigned)((L.nchunks - 1) * 2 * T * q.ny), 128, 0, q.stream>>>(u);
+        count_launch();
+    }
+    if (L.wx2 > 0) {
+        k_unstash_x<<<(unsigned)(depth_ * q.ny), 64, 0, q.stream>>>(u);
+        count_launch();
+    }
+    rc = check_launch("k_unstash");
     return rc;
 }
 
@@ -661,17 +692,22 @@ static int dispatch(int levels, const LaunchReq &q) {
     case 2:
         switch (idx) {
         case 1: return launch_cfg<2, 32, 4, 4>(q);
+        case 2: return launch_cfg<2, 16, 2, 4>(q);
+        case 3: return launch_cfg<2, 24, 2, 4>(q);
         default: return launch_cfg<2, 32, 4, 6>(q);
         }
     case 3:
         switch (idx) {
         case 1: return launch_cfg<3, 32, 4, 3>(q);
+        case 2: return launch_cfg<3, 16, 2, 4>(q);
+        case 3: return launch_cfg<3, 24, 2, 4>(q);
         default: return launch_cfg<3, 32, 4, 5>(q);
         }
     case 4:
         switch (idx) {
         case 1: return launch_cfg<4, 32, 4, 3>(q);
-        case 2: return launch_cfg<4, 32, 4, 5>(q);
+        case 2: return launch_cfg<4, 16, 2, 4>(q);
+        case 3: return launch_cfg<4, 24, 2, 4>(q);
         default: return launch_cfg<4, 32, 4, 4>(q);
         }
     default:

@@ -1,2 +1,3 @@
 #!/bin/bash
-for t in 2 3 4; do for c in 0 1; do python tools/prof_kernel.py --t $t --cfg $c --reps 5; done; done 2>&1 | grep -v Warn
+for t in 2 3 4; do timeout 60 python tools/prof_kernel.py --t $t --reps 5; done 2>&1 | grep -v Warn
+timeout 120 python tools/prof_c3.py 600 16 4 2>&1 | grep GLUP
