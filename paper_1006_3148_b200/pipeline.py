@@ -291,7 +291,7 @@ class PipelineEngine:
         return self._rings_equal
 
     # -- passes ---------------------------------------------------------------
-    def _pass_two_grid(self, direction):
+    def _pass_two_grid(self, direction, boundary=None):
         cfg = self.cfg
         h = cfg.h
         lives = self._lives(h)
@@ -307,10 +307,29 @@ class PipelineEngine:
         cur, other = self.grids[L0 % 2], self.grids[(L0 + 1) % 2]
         u0 = 0
         launches = 0
-        for c in split_levels(h, self.max_fused):
+        chunks = split_levels(h, self.max_fused)
+        for n, c in enumerate(chunks):
             zlo, zhi = lives[u0 + c][2]
-            fused_sweeps(cur, other, c, zlo, zhi)
-            launches += 1
+            last = n == len(chunks) - 1
+            if last and boundary is not None and zhi - zlo > boundary[0] + boundary[1]:
+                # boundary-first: the planes the halo exchange sends are
+                # finished first, the exchange is posted, and the interior
+                # planes are computed while the transfer is in flight
+                blo, bhi, post = boundary
+                if blo:
+                    fused_sweeps(cur, other, c, zlo, zlo + blo)
+                    launches += 1
+                if bhi:
+                    fused_sweeps(cur, other, c, zhi - bhi, zhi)
+                    launches += 1
+                post(other.data, other.offset)
+                fused_sweeps(cur, other, c, zlo + blo, zhi - bhi)
+                launches += 1
+            else:
+                fused_sweeps(cur, other, c, zlo, zhi)
+                launches += 1
+                if last and boundary is not None:
+                    boundary[2](other.data, other.offset)
             cur, other = other, cur
             u0 += c
         target = self.grids[(L0 + h) % 2]
@@ -363,10 +382,16 @@ class PipelineEngine:
             self._ws = ws
         return ws[(levels, depth)]
 
-    def run_pass(self, direction: int) -> RunStats:
+    def run_pass(self, direction: int, boundary=None) -> RunStats:
         """One team sweep: every interior cell receives h updates
         (sp/pipeline.py:451-519).  Stream-ordered: the kernels are enqueued on
-        the current CUDA stream; results are visible to later stream work."""
+        the current CUDA stream; results are visible to later stream work.
+
+        `boundary` = (planes_low, planes_high, post): two-grid fused passes
+        finish the lowest / highest z planes of the last level first and call
+        post(storage, offset) before computing the rest (used by the z-slab
+        driver to overlap the halo exchange with interior compute).  Without
+        the fused path, post is called after the pass."""
         cfg = self.cfg
         if direction not in (1, -1):
             raise ValueError("direction must be +1 or -1")
@@ -381,7 +406,7 @@ class PipelineEngine:
                     f"backward pass needs alignment >= h ({a0} < {cfg.h})")
             launches = self._pass_compressed(direction)
         else:
-            launches = self._pass_two_grid(direction)
+            launches = self._pass_two_grid(direction, boundary)
         self.levels_done += cfg.h
         self.passes_done += 1
         if cfg.grid_mode == "compressed":

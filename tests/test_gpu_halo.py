@@ -30,7 +30,13 @@ def _emulate(dc):
     for c in range(dc.cycles):
         direction = 1 if c % 2 == 0 else -1
         for rt in rts:
-            rt.engine.run_pass(direction)
+            # boundary-first split of the last fused chunk (the overlap path of
+            # RankRuntime.cycle); the post hook only records the call here
+            lo_nb, hi_nb = rt.sub.has_nb[2]
+            seen = []
+            bnd = (rt.sub.h if lo_nb else 0, rt.sub.h if hi_nb else 0,
+                   lambda data, off: seen.append(off))
+            rt.engine.run_pass(direction, bnd if dc.cfg.grid_mode == "two_grid" else None)
             rt.sub.grid = rt.engine.current_grid()
         for axis in range(3):
             staged = []

@@ -57,7 +57,7 @@ class OracleEngine:
             return self.grids[0]
         return self.grids[self.levels_done % 2]
 
-    def run_pass(self, direction):
+    def run_pass(self, direction, boundary=None):
         h = self.cfg.h
         if self.cfg.grid_mode == "two_grid":
             for u in range(1, h + 1):
@@ -81,6 +81,9 @@ class OracleEngine:
                 self._faces_at(d, do, dims, full=False, win=win)
             g.alignment = a0 + s * h
         self.levels_done += h
+        if boundary is not None:
+            cur = self.current_grid()
+            boundary[2](cur.data, cur.offset)
 
     # Dirichlet faces at a frame, physical sides only (sp/pipeline.py:427-447)
     def _faces_at(self, d, off, dims, full, win=None):

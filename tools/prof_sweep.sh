@@ -1,3 +1,2 @@
 #!/bin/bash
 for t in 2 3 4; do timeout 60 python tools/prof_kernel.py --t $t --reps 5; done 2>&1 | grep -v Warn
-timeout 120 python tools/prof_c3.py 600 16 4 2>&1 | grep GLUP
