@@ -149,7 +149,7 @@ int sp_compressed(double *data, int64_t ex, int64_t ey, int64_t ez,
  * key 0: z-chunk length for sp_sweep / sp_temporal (0 = automatic)
  * key 1: force the cp.async (non-TMA) loader when nonzero
  * key 2: tile config index per fused depth (value = levels*16 + index)
- * key 3: relaxed inter-warp synchronisation in sp_temporal (0/1) */
+ * key 4: profiling knobs (only in builds with -DSP200_PROFILE_KNOBS=1) */
 int sp_set_tuning(int key, int64_t value);
 
 /* Query: 1 if the TMA loader applies to a grid with row extent `ex`. */

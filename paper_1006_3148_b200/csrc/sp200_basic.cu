@@ -263,7 +263,6 @@ int sp_set_tuning(int key, int64_t value) {
     switch (key) {
     case 0: t.zchunk = value; return SP_OK;
     case 1: t.force_cpasync = value; return SP_OK;
-    case 3: t.relaxed_sync = value; return SP_OK;
     case 4: t.debug = value; return SP_OK;
     case 2: {
         int lv = (int)(value / 16), idx = (int)(value % 16);

@@ -94,29 +94,4 @@ __device__ __forceinline__ void cp_async_wait() {
 // Streaming (evict-first) store: the output plane is not re-read by this pass.
 __device__ __forceinline__ void st_stream(double *p, double v) { __stcs(p, v); }
 
-// Shared-memory progress flags for inter-warp relaxed synchronisation.
-__device__ __forceinline__ unsigned ld_acquire_cta(const unsigned *p) {
-    unsigned v;
-    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_cta(unsigned *p, unsigned v) {
-    asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
-}
-
-// Global-memory progress flags between CTAs (K3 in-place ordering).
-__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_gpu(unsigned *p, unsigned v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-// Relaxed publish: the published fact (a TMA load has landed) needs no
-// ordering of this thread's earlier writes, so no release fence is paid.
-__device__ __forceinline__ void st_relaxed_gpu(unsigned *p, unsigned v) {
-    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
 }  // namespace sp200

@@ -18,7 +18,6 @@ struct Tuning {
     int64_t zchunk = 0;     // 0 = automatic
     int64_t force_cpasync = 0;
     int64_t cfg_index[SP_MAX_FUSED + 1] = {0, 0, 0, 0, 0};
-    int64_t relaxed_sync = 0;
     int64_t debug = 0;
 };
 Tuning &tuning();

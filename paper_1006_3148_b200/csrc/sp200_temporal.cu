@@ -31,6 +31,12 @@
 #include <type_traits>
 
 #include "sp200_device.cuh"
+
+// Profiling-only switches (sp_set_tuning key 4) that skip parts of the fused
+// pass to attribute time; compiled out of the product build.
+#ifndef SP200_PROFILE_KNOBS
+#define SP200_PROFILE_KNOBS 0
+#endif
 #include "sp200_internal.h"
 
 namespace sp200 {
@@ -43,6 +49,7 @@ struct TParams {
     int ox, ex0;   // stored tile width; region column of the first stored column
     int pair_store;  // 16-byte aligned column pairs in global memory
     int tiles_x, tiles_y, ntiles;
+    int tile_base, tile_count;  // tiles [tile_base, tile_base+tile_count) in this launch
     int zlo, zhi, zc;
     int doff;        // storage offset of logical 0 in the written frame
     int direction;   // K3: +1 forward (write shifted -T), -1 backward
@@ -144,8 +151,8 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     // one (tile, z-chunk) unit per CTA, tile-fastest so that concurrently
     // running CTAs cover neighbouring tiles at the same z range and the
     // overlapped halo reads hit L2
-    const int tile = blockIdx.x % p.ntiles;
-    const int chunk = blockIdx.x / p.ntiles;
+    const int tile = p.tile_base + (int)(blockIdx.x % p.tile_count);
+    const int chunk = (int)(blockIdx.x / p.tile_count);
     const int z0 = p.zlo + chunk * p.zc;
     const int z1 = min(z0 + p.zc, p.zhi);
     const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
@@ -234,7 +241,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     };
 
     if constexpr (TMA) {
-        if (tid == 0 && !(p.debug & 2))
+        if (tid == 0 && !(SP200_PROFILE_KNOBS && (p.debug & 2)))
             for (int s = 0; s < S - 1; ++s)
                 if (s < nload) issue(s);
     } else {
@@ -376,13 +383,13 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     auto one_step = [&](int s, auto Qc) {
         const int si = (int)((gbase + s) % S);
         if constexpr (TMA) {
-            if (s < nload && !(p.debug & 2)) mbar_wait(&bar[si], (uint32_t)(((gbase + s) / S) & 1));
+            if (s < nload && !(SP200_PROFILE_KNOBS && (p.debug & 2))) mbar_wait(&bar[si], (uint32_t)(((gbase + s) / S) & 1));
         } else {
             cp_async_wait<S - 2>();
         }
-        if (!(p.debug & 4)) __syncthreads();
+        if (!(SP200_PROFILE_KNOBS && (p.debug & 4))) __syncthreads();
         if constexpr (TMA) {
-            if (tid == 0 && s + S - 1 < nload && !(p.debug & 2)) issue(s + S - 1);
+            if (tid == 0 && s + S - 1 < nload && !(SP200_PROFILE_KNOBS && (p.debug & 2))) issue(s + S - 1);
         } else {
             if (s + S - 1 < nload) issue(s + S - 1);
             else cp_async_commit();
@@ -391,7 +398,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
         // every level's finished plane inside [0, nz): no z-ring this step
         const int pmax = z0 - T + s - 1, pmin = z0 - T + s - 2 * T + 1;
         const bool zall = (pmin >= 0) && (pmax < p.nz);
-        if (p.debug & 1) return;  // profiling only: skip the level updates
+        if (SP200_PROFILE_KNOBS && (p.debug & 1)) return;  // profiling builds only
         if (wint && zall) levels(s, cur, Qc, IC<0>{});
         else if (zall) levels(s, cur, Qc, IC<1>{});
         else levels(s, cur, Qc, IC<2>{});
@@ -626,6 +633,8 @@ static int launch_cfg(const LaunchReq &q) {
         p.zc = (int)zc;
         grid = (int64_t)p.ntiles * ((depth + zc - 1) / zc);
     }
+    p.tile_base = 0;
+    p.tile_count = p.ntiles;
     if (grid > 0x7fffffff) return set_error(SP_EUNSUP, "grid too large");
 
     CUtensorMap tmap;
@@ -640,6 +649,31 @@ static int launch_cfg(const LaunchReq &q) {
                                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return set_error(SP_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    }
+    if (!comp && tuning().zchunk <= 0 && p.ntiles >= slots) {
+        // Two launches: whole slots-worth of tiles march their full column
+        // (no pipeline restarts), the remaining tiles are split into z-chunks
+        // so that together they fill one more wave.  Both keep neighbouring
+        // tiles at the same z at the same time (L2 catches the halos).
+        const int full = (int)((p.ntiles / slots) * slots);
+        const int rem = p.ntiles - full;
+        TParams a = p;
+        a.tile_base = 0;
+        a.tile_count = full;
+        a.zc = (int)depth;
+        kern<<<(unsigned)full, C::NT, C::SMEM, q.stream>>>(a, tmap);
+        count_launch();
+        int rc = check_launch("k_temporal");
+        if (rc || rem == 0) return rc;
+        TParams b = p;
+        b.tile_base = full;
+        b.tile_count = rem;
+        const int64_t zcb = pick_zchunk(depth, rem, slots, T);
+        b.zc = (int)zcb;
+        const int64_t gb = (int64_t)rem * ((depth + zcb - 1) / zcb);
+        kern<<<(unsigned)gb, C::NT, C::SMEM, q.stream>>>(b, tmap);
+        count_launch();
+        return check_launch("k_temporal");
     }
     kern<<<(unsigned)grid, C::NT, C::SMEM, q.stream>>>(p, tmap);
     count_launch();

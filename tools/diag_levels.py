@@ -9,7 +9,6 @@ def one(levels, loader, dims):
     import oracle, paper_1006_3148_b200 as sp
     L = sp._lib.load()
     L.sp_set_tuning(1, 1 if loader == "cpasync" else 0)
-    L.sp_set_tuning(3, int(os.environ.get("SP_RELAX", "0")))
     d0 = oracle.make_storage(*dims, init="random", seed=7, ring=0.75)
     src = sp.Grid3.from_numpy(*dims, 0, d0)
     dst = src.copy()
