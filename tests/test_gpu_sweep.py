@@ -176,3 +176,47 @@ def test_large_config_c1(golden):
     g = sp.create_grid(*c["n"], init="random", seed=c["seed"], ring=c["ring"])
     assert g.checksum() == c["init_digest"]
     assert _sweeps(g, c["sweeps"]).checksum() == c["digest"]
+
+
+def test_layout_extents_alignment_and_faces():
+    """Storage layout of sp/grid.py:47-120: extents include pad, x fastest,
+    logical (i,j,k) at pad+1-alignment+(k,j,i), faces captured per axis."""
+    g = sp.create_grid(4, 4, 4, pad=2, init="constant", value=1.0)
+    assert tuple(g.data.shape) == (8, 8, 8) and bool(torch.all(g.data == 1.0))
+    g = sp.create_grid(5, 4, 3, pad=0)
+    assert g.data.stride() == (6 * 7, 7, 1)
+    g = sp.create_grid(6, 6, 6, pad=2, init="random", seed=3)
+    before = g.interior_numpy().copy()
+    g.alignment = 1  # frame moves one cell toward lower storage indices
+    assert g.index(0, 0, 0) == (2, 2, 2)
+    g.data[2:8, 2:8, 2:8] = torch.from_numpy(before).cuda()
+    assert_bitwise(g.interior_numpy(), before)
+    g.capture_boundary_faces()
+    assert g.boundary_faces[("x", 0)].shape == (6, 6)
+    assert g.boundary_faces[("z", 1)].shape == (6, 6)
+
+
+def test_snapshots_are_byte_identical_across_runs(tmp_path):
+    """Acceptance #8 (tests/test_acceptance.py:266-280): two identical runs
+    produce byte-identical snapshots; the snapshot equals the oracle's."""
+    import oracle
+    outs = []
+    for k in range(2):
+        g = sp.create_grid(37, 29, 23, init="random", seed=99, ring=0.5)
+        cfg = sp.PipelineConfig(spec=sp.BlockSpec(37, 8, 8), t=3)
+        st = sp.run_pipelined((g, g.copy()), cfg, 3)
+        path = tmp_path / f"snap{k}.bin"
+        sp.write_snapshot(st.result, path)
+        outs.append(path.read_bytes())
+    assert outs[0] == outs[1]
+    d0 = oracle.make_storage(37, 29, 23, init="random", seed=99, ring=0.5)
+    exp = oracle.interior(oracle.sweeps(d0, (37, 29, 23), 9), 37, 29, 23)
+    assert outs[0] == b"37 29 23\n" + exp.astype("<f8").tobytes()
+
+
+def test_no_cpu_fallback_without_library(monkeypatch):
+    """The product path fails loudly when the CUDA library is missing."""
+    from paper_1006_3148_b200 import _lib
+    monkeypatch.setattr(_lib, "_lib", None)
+    with pytest.raises(ImportError):
+        _lib.load("/nonexistent/libsp200.so")
