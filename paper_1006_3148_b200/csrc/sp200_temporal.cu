@@ -159,8 +159,12 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     const int x0 = tx * p.ox, y0 = ty * C::OY;
     const int rx0 = x0 - p.ex0, ry0 = y0 - (T - 1);  // logical coords of region (0, 0)
 
+    // Dirichlet ring cells keep their value at every level; cells beyond the
+    // ring are computed but never read by a kept cell, so only the ring
+    // column of a lane (x = -1 or nx) and the ring rows of a warp (y = -1 or
+    // ny, warp-uniform) need the select
     bool x_out[2];
-    unsigned okb = 0;   // bit 2r+c: cell (row r, column c) is an interior cell in x and y
+    unsigned ringb = 0;  // bit 2r+c: cell (row r, column c) is a ring cell
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
         const int xc = rx0 + i0 + c, ic = i0 + c;
@@ -168,7 +172,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int y = ry0 + j0 + r;
-            if (xc >= 0 && xc < p.nx && y >= 0 && y < p.ny) okb |= 1u << (2 * r + c);
+            if (xc == -1 || xc == p.nx || y == -1 || y == p.ny) ringb |= 1u << (2 * r + c);
         }
     }
     bool y_out[R];
@@ -177,8 +181,8 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
         const int jr = j0 + r, y = ry0 + jr;
         y_out[r] = (jr >= T - 1) && (jr < T - 1 + C::OY) && (y < p.ny);
     }
-    // warps whose cells are all interior in x and y skip the Dirichlet select
-    const bool wint = __all_sync(0xffffffffu, okb == (1u << (2 * R)) - 1u);
+    // warps without ring cells skip the select
+    const bool wint = !__any_sync(0xffffffffu, ringb != 0u);
 
     const int nload = (z1 - z0) + 2 * T;      // level-0 planes z0-T .. z1+T-1
     const int nsteps = (z1 - z0) + 3 * T - 1;  // level T emits plane z0+s-3T+1 at step s
@@ -264,7 +268,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
         for (int u = T; u >= 1; --u) {
             const int ui = (u > 1) ? u - 2 : 0;
             const int pout = z0 - T + s - 2 * u + 1;
-            const bool z_in = (pout >= 0) && (pout < p.nz);
+            const bool z_ring = (pout == -1) || (pout == p.nz);
             const double *B = (u == 1) ? cur : lev + ((u - 2) * 2 + (Q ^ 1)) * PLANE_AL;
             if (u == 1) {
 #pragma unroll
@@ -324,10 +328,11 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
                 for (int c = 0; c < 2; ++c) {
                     const double wl = (u == 1) ? st.W0[Q ^ 1][r][c] : st.P[ui][Q][r][c];
                     v[r][c] = dmul(v[r][c], 1.0 / 6.0);
+                    // level T values are stored only for interior cells
                     if constexpr (MODE == 1) {
-                        if (!((okb >> (2 * r + c)) & 1u)) v[r][c] = wl;
+                        if (u < T && ((ringb >> (2 * r + c)) & 1u)) v[r][c] = wl;
                     } else if constexpr (MODE == 2) {
-                        if (!(((okb >> (2 * r + c)) & 1u) && z_in)) v[r][c] = wl;
+                        if (u < T && (((ringb >> (2 * r + c)) & 1u) || z_ring)) v[r][c] = wl;
                     }
                     st.Sp[u - 1][r][c] = dadd(n[r][c], wl);
                     if (u < T) st.P[u < T ? u - 1 : 0][Q][r][c] = v[r][c];
