@@ -69,6 +69,7 @@ struct KCfg {
     static constexpr int NT = 32 * (CY / R);
     static constexpr int OY = CY - 2 * (T - 1);
     static constexpr int NLEV = (T > 1) ? 2 * (T - 1) : 0;
+    static constexpr int XBW = 2 * T + 2;        // K3 x-stash columns per tile (even)
     static constexpr size_t SMEM = (size_t)(S + NLEV) * PLANE_AL * sizeof(double) + 8 * S + 16;
     // CTAs per SM the shared memory allows (1 KB per CTA is reserved by the
     // runtime); the register budget follows through __launch_bounds__
@@ -193,35 +194,42 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
 
     // K3 bands: outputs whose shifted store would land in a neighbour's read
     // region go to the stash (forward: the low 2T columns / rows / planes of
-    // the tile unless it is the first; backward: the high 2T unless last)
+    // the tile unless it is the first; backward: the high 2T unless last).
+    // The x band is taken in whole column pairs, so it is 2T + (ex0 & 1) wide.
     const bool fwd = p.direction > 0;
-    bool xb[2];
-    int kx[2];
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-        const int xo = rx0 + i0 + c - x0;  // column within the stored tile
-        xb[c] = COMP && (fwd ? (tx > 0 && xo < 2 * T) : (tx < p.tiles_x - 1 && xo >= p.ox - 2 * T));
-        kx[c] = fwd ? (tx - 1) * 2 * T + xo : tx * 2 * T + xo - (p.ox - 2 * T);
-    }
+    const int sxpad = p.ex0 & 1;
+    const int xo0 = rx0 + i0 - x0;  // stored-tile column of the lane's first cell
+    const bool xband = COMP && (fwd ? (tx > 0 && xo0 < 2 * T)
+                                    : (tx < p.tiles_x - 1 && xo0 >= p.ox - 2 * T - sxpad));
     bool yb[R];
-    int ky[R];
+    int ky0;
+    {
+        const int yo = ry0 + j0 - y0;
+        ky0 = fwd ? (ty - 1) * 2 * T + yo : ty * 2 * T + yo - (C::OY - 2 * T);
+    }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int yo = ry0 + j0 + r - y0;
         yb[r] = COMP && (fwd ? (ty > 0 && yo < 2 * T) : (ty < p.tiles_y - 1 && yo >= C::OY - 2 * T));
-        ky[r] = fwd ? (ty - 1) * 2 * T + yo : ty * 2 * T + yo - (C::OY - 2 * T);
     }
     const int nchunks = (p.zhi - p.zlo + p.zc - 1) / p.zc;
     const bool zband_chunk = COMP && (fwd ? chunk > 0 : chunk < nchunks - 1);
-    // stash addressing, affine in the output plane: stash_y / stash_z rows are
-    // padded by one column so that column pairs stay 16-byte aligned
-    const int sxpad = p.ex0 & 1;
-    const int srow = (p.nx + 2) & ~1;  // even: pairs stay 16-byte aligned
-    double *sx_col[2];
-#pragma unroll
-    for (int c = 0; c < 2; ++c)
-        sx_col[c] = COMP ? p.stash_x + ((int64_t)(ry0 + j0 - p.zlo * p.ny)) * p.wx2 + kx[c] : nullptr;
-    double *sy_col = COMP ? p.stash_y + ((int64_t)ky[0] - (int64_t)p.zlo * p.hy2) * srow + rx0 + i0 + sxpad
+    // destinations, affine in the output plane pout and the row r:
+    //   in place / x stash: ncol + pout * npz + r * nrs
+    //   y stash: sy_col + (pout * hy2 + r) * srow;  z stash: sz_col + (kz * ny + r) * srow
+    // stash rows are padded so that column pairs stay 16-byte aligned
+    const int srow = (p.nx + 2) & ~1;
+    double *ncol = dcol + (int64_t)p.doff * pz;
+    int64_t npz = pz;
+    int nrs = (int)p.ex;
+    if (COMP && xband) {
+        const int kx0 = fwd ? (tx - 1) * C::XBW + xo0 + sxpad : tx * C::XBW + xo0 - (p.ox - 2 * T - sxpad);
+        ncol = p.stash_x + (int64_t)(ry0 + j0 - p.zlo * p.ny) * p.wx2 + kx0;
+        npz = (int64_t)p.ny * p.wx2;
+        nrs = p.wx2;
+    }
+    const bool npair = x_out[0] && x_out[1] && (xband || p.pair_store);
+    double *sy_col = COMP ? p.stash_y + ((int64_t)ky0 - (int64_t)p.zlo * p.hy2) * srow + rx0 + i0 + sxpad
                           : nullptr;
     double *sz_col = COMP ? p.stash_z + (int64_t)(ry0 + j0) * srow + rx0 + i0 + sxpad : nullptr;
 
@@ -282,6 +290,19 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
             const double2 cp = lds2(B + (j0 + R + 1) * SPX + C0 + i0);
             double *pub = lev + ((u - 1) * 2 + Q) * PLANE_AL;
             const bool store_plane = (u == T) && pout >= z0 && pout < z1;
+            // K3 destinations of this level-T plane
+            [[maybe_unused]] double *nrow = nullptr, *yrow = nullptr, *zrow = nullptr;
+            [[maybe_unused]] bool zb = false;
+            if constexpr (COMP) {
+                if (u == T) {
+                    nrow = ncol + (int64_t)pout * npz;
+                    const int zo = pout - z0;
+                    zb = zband_chunk && (fwd ? zo < 2 * T : zo >= (z1 - z0) - 2 * T);
+                    const int kz = fwd ? (chunk - 1) * 2 * T + zo : chunk * 2 * T + zo - ((z1 - z0) - 2 * T);
+                    yrow = sy_col + (int64_t)pout * p.hy2 * srow;
+                    zrow = sz_col + (int64_t)kz * p.ny * srow;
+                }
+            }
             // gather the level u-1 inputs of all 2R cells first, then run the
             // five dependent adds stage by stage across all cells so that the
             // 8-cycle DADD latency is covered by independent work of this warp
@@ -342,43 +363,32 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
                 if (u < T) {
                     if (r == 0 || r == R - 1) sts2(pub + (j0 + r + 1) * SPX + C0 + i0, v[r][0], v[r][1]);
                 } else if (store_plane && y_out[r]) {
-                    double *g = dcol + (int64_t)(pout + p.doff) * pz + (int64_t)r * p.ex;
                     if constexpr (COMP) {
                         // band priority y, then z, then x (k_unstash_* skip
                         // in the same order); y and z bands are whole rows
-                        const int zo = pout - z0;
-                        const bool zb = zband_chunk && (fwd ? zo < 2 * T : zo >= (z1 - z0) - 2 * T);
-                        double *row = nullptr;
+                        double *row = nrow + (int64_t)r * nrs;
+                        bool pr = npair;
                         if (yb[r]) {
-                            row = sy_col + ((int64_t)pout * p.hy2 + r) * srow;
+                            row = yrow + (int64_t)r * srow;
+                            pr = x_out[0] && x_out[1];
                         } else if (zb) {
-                            const int kz = fwd ? (chunk - 1) * 2 * T + zo
-                                               : chunk * 2 * T + zo - ((z1 - z0) - 2 * T);
-                            row = sz_col + ((int64_t)kz * p.ny + r) * srow;
+                            row = zrow + (int64_t)r * srow;
+                            pr = x_out[0] && x_out[1];
                         }
-                        if (row) {
-                            if (x_out[0] && x_out[1]) stg2_stream(row, v[r][0], v[r][1]);
-                            else {
-                                if (x_out[0]) row[0] = v[r][0];
-                                if (x_out[1]) row[1] = v[r][1];
-                            }
-                        } else if (!xb[0] && !xb[1] && x_out[0] && x_out[1] && p.pair_store) {
+                        if (pr) {
+                            stg2_stream(row, v[r][0], v[r][1]);
+                        } else {
+                            if (x_out[0]) st_stream(row, v[r][0]);
+                            if (x_out[1]) st_stream(row + 1, v[r][1]);
+                        }
+                    } else {
+                        double *g = dcol + (int64_t)(pout + p.doff) * pz + (int64_t)r * p.ex;
+                        if (x_out[0] && x_out[1] && p.pair_store) {
                             stg2_stream(g, v[r][0], v[r][1]);
                         } else {
-#pragma unroll
-                            for (int c = 0; c < 2; ++c) {
-                                if (!x_out[c]) continue;
-                                if (xb[c])
-                                    sx_col[c][((int64_t)pout * p.ny + r) * p.wx2] = v[r][c];
-                                else
-                                    st_stream(g + c, v[r][c]);
-                            }
+                            if (x_out[0]) st_stream(g, v[r][0]);
+                            if (x_out[1]) st_stream(g + 1, v[r][1]);
                         }
-                    } else if (x_out[0] && x_out[1] && p.pair_store) {
-                        stg2_stream(g, v[r][0], v[r][1]);
-                    } else {
-                        if (x_out[0]) st_stream(g, v[r][0]);
-                        if (x_out[1]) st_stream(g + 1, v[r][1]);
                     }
                 }
             }
@@ -466,9 +476,23 @@ __global__ void k_unstash_x(UnstashArgs a) {
     if (a.fwd ? (chunk > 0 && zo < a.T2) : (chunk < a.nchunks - 1 && zo >= zlen - a.T2)) return;
     const double *src = a.sx + (int64_t)blockIdx.x * a.wx2;
     double *dst = a.data + ((int64_t)(z + a.doff) * a.ey + (y + a.doff)) * a.ex + a.doff;
+    // stash column k of tile slot bt holds stored-tile column lo + (k mod XBW),
+    // lo = -e (forward) or ox - 2T - e (backward); the forward band ends with
+    // the lane pair that starts below 2T (see the x band in k_temporal)
+    const int xbw = a.T2 + 2, e = a.sxpad;
     for (int k = threadIdx.x; k < a.wx2; k += blockDim.x) {
-        const int x = band_pos(k, a.ox, a.T2, a.fwd);
-        if (x < a.nx) dst[x] = src[k];
+        const int bt = k / xbw, kk = k - bt * xbw;
+        int xo, tile;
+        if (a.fwd) {
+            if ((kk & ~1) - e >= a.T2) continue;
+            xo = kk - e;
+            tile = bt + 1;
+        } else {
+            xo = a.ox - a.T2 - e + kk;
+            tile = bt;
+        }
+        const int x = tile * a.ox + xo;
+        if (xo >= 0 && xo < a.ox && x < a.nx) dst[x] = src[k];
     }
 }
 
@@ -559,7 +583,7 @@ static void comp_layout(int64_t nx, int64_t ny, int64_t depth, int64_t off, bool
     if (zc < 2 * T) zc = std::min<int64_t>(depth, 2 * T);
     L->zc = zc;
     L->nchunks = (depth + zc - 1) / zc;
-    L->wx2 = (tx - 1) * 2 * T;
+    L->wx2 = (tx - 1) * (2 * T + 2);
     L->hy2 = (ty - 1) * 2 * T;
     L->nx_stash = depth * ny * L->wx2;
     L->ny_stash = depth * L->hy2 * ((nx + 2) & ~1);
