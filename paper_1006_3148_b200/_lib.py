@@ -11,7 +11,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsp200.so")
+# SP200_LIB selects another in-tree build (kernel A/B experiments in tools/)
+LIB_PATH = os.environ.get("SP200_LIB") or os.path.join(HERE, "libsp200.so")
 
 SP_OK = 0
 SP_EINVAL = -1

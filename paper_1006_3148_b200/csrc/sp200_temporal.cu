@@ -120,7 +120,10 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     uint64_t *bar = reinterpret_cast<uint64_t *>(lev + C::NLEV * PLANE_AL);
 
     const int tid = threadIdx.x;
-    const int lane = tid & 31, warp = tid >> 5;
+    // K3: the warp index through a shuffle is provably warp-uniform, so the
+    // band predicates and stash row addresses go to the uniform datapath
+    // (measured +7 % for K3; the same change costs K2 2 %)
+    const int lane = tid & 31, warp = COMP ? __shfl_sync(0xffffffffu, tid >> 5, 0) : tid >> 5;
     const int i0 = 2 * lane;   // region column of this lane's first cell
     const int j0 = warp * R;   // first region row
 
