@@ -470,32 +470,40 @@ __global__ void k_unstash_z(UnstashArgs a) {
 }
 
 __global__ void k_unstash_x(UnstashArgs a) {
-    const int y = blockIdx.x % a.ny, zr = blockIdx.x / a.ny;
+    // one warp per (y, z) row; lane -> (tile slot offset, column in the slot)
+    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int nrows = (a.zhi - a.zlo) * a.ny;
+    if (row >= nrows) return;
+    const int y = row % a.ny, zr = row / a.ny;
     const int z = a.zlo + zr;
     const int ty = y / a.oy;
     if (band_hit(y - ty * a.oy, ty, a.tiles_y, a.oy, a.T2, a.fwd)) return;
     const int zo = zr % a.zc, chunk = zr / a.zc;
     const int zlen = min(a.zc, a.zhi - a.zlo - chunk * a.zc);
     if (a.fwd ? (chunk > 0 && zo < a.T2) : (chunk < a.nchunks - 1 && zo >= zlen - a.T2)) return;
-    const double *src = a.sx + (int64_t)blockIdx.x * a.wx2;
+    const double *src = a.sx + (int64_t)row * a.wx2;
     double *dst = a.data + ((int64_t)(z + a.doff) * a.ey + (y + a.doff)) * a.ex + a.doff;
-    // stash column k of tile slot bt holds stored-tile column lo + (k mod XBW),
+    // stash column kk of tile slot bt holds stored-tile column lo + kk,
     // lo = -e (forward) or ox - 2T - e (backward); the forward band ends with
     // the lane pair that starts below 2T (see the x band in k_temporal)
     const int xbw = a.T2 + 2, e = a.sxpad;
-    for (int k = threadIdx.x; k < a.wx2; k += blockDim.x) {
-        const int bt = k / xbw, kk = k - bt * xbw;
-        int xo, tile;
-        if (a.fwd) {
-            if ((kk & ~1) - e >= a.T2) continue;
-            xo = kk - e;
-            tile = bt + 1;
-        } else {
-            xo = a.ox - a.T2 - e + kk;
-            tile = bt;
-        }
-        const int x = tile * a.ox + xo;
-        if (xo >= 0 && xo < a.ox && x < a.nx) dst[x] = src[k];
+    const int per = 32 / xbw, lane = threadIdx.x & 31;
+    const int boff = lane / xbw, kk = lane - boff * xbw;
+    if (boff >= per) return;
+    int xo;
+    bool ok;
+    if (a.fwd) {
+        ok = (kk & ~1) - e < a.T2;
+        xo = kk - e;
+    } else {
+        ok = true;
+        xo = a.ox - a.T2 - e + kk;
+    }
+    ok = ok && xo >= 0 && xo < a.ox;
+    const int nslots = a.wx2 / xbw;
+    for (int bt = boff; bt < nslots; bt += per) {
+        const int x = (a.fwd ? bt + 1 : bt) * a.ox + xo;
+        if (ok && x < a.nx) dst[x] = src[bt * xbw + kk];
     }
 }
 
@@ -744,7 +752,7 @@ static int launch_cfg(const LaunchReq &q) {
         count_launch();
     }
     if (L.wx2 > 0) {
-        k_unstash_x<<<(unsigned)(depth_ * q.ny), 64, 0, q.stream>>>(u);
+        k_unstash_x<<<(unsigned)((depth_ * q.ny + 7) / 8), 256, 0, q.stream>>>(u);
         count_launch();
     }
     rc = check_launch("k_unstash");
