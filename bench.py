@@ -345,6 +345,30 @@ def run_ours(args):
                                   "wall_s": st3.wall_seconds,
                                   "config": "600^3 in 606^3 (pad 4), t=4 x16 passes, in place"}
         del g3
+        # C5 on one GPU: 2048^3 global, two 2050^3 grids = 137.8 GB of HBM,
+        # 32 sweeps at t=4 (8 passes), device-timed with CUDA events
+        torch.cuda.empty_cache()
+        if torch.cuda.mem_get_info()[0] >= 140e9:
+            n5 = 2048
+            a5 = sp.create_grid(n5, n5, n5, init="random", seed=SEED)
+            b5 = a5.copy()
+            cfg5 = sp.PipelineConfig(spec=sp.BlockSpec(n5, 32, 32), t=4)
+            sp.run_pipelined((a5, b5), cfg5, 2)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            sp.run_pipelined((a5, b5), cfg5, 8)
+            e1.record()
+            torch.cuda.synchronize()
+            ms5 = e0.elapsed_time(e1)
+            extra["C5_single_gpu"] = {
+                "glups": n5 ** 3 * 32 / (ms5 / 1e3) / 1e9, "ms": ms5, "sweeps": 32,
+                "hbm_gb_resident": 2 * a5.data.numel() * 8 / 1e9,
+                "config": "2048^3 in 2050^3, two grids, t=4 x8 passes, U[0,1) seed 42, ring 0.0"}
+            del a5, b5
+            torch.cuda.empty_cache()
+        else:
+            extra["C5_single_gpu"] = {"skipped": "needs 140 GB of free HBM"}
 
     # --- e2e through the public API with host buffers --------------------------
     e2e = None

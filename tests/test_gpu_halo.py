@@ -24,32 +24,9 @@ def _box(g, box):
 
 
 def _emulate(dc):
-    gd = dc.resolved_global()
-    subs = halo.decompose_domain(gd, dc.topo, halo.HaloSpec(dc.cfg.h))
-    rts = [halo.RankRuntime(s, dc.cfg, None, seed=dc.seed, ring=dc.ring) for s in subs]
-    for c in range(dc.cycles):
-        direction = 1 if c % 2 == 0 else -1
-        for rt in rts:
-            # boundary-first split of the last fused chunk (the overlap path of
-            # RankRuntime.cycle); the post hook only records the call here
-            lo_nb, hi_nb = rt.sub.has_nb[2]
-            seen = []
-            bnd = (rt.sub.h if lo_nb else 0, rt.sub.h if hi_nb else 0,
-                   lambda data, off: seen.append(off))
-            rt.engine.run_pass(direction, bnd if dc.cfg.grid_mode == "two_grid" else None)
-            rt.sub.grid = rt.engine.current_grid()
-        for axis in range(3):
-            staged = []
-            for rt in rts:
-                for m in rt.plan.messages:
-                    if m.axis == axis:
-                        staged.append((m.neighbor, m, _box(rt.sub.grid, m.send_box).clone()))
-            for nb, m, payload in staged:
-                dst = rts[nb]
-                # the receiver's message from this sender sits on the opposite side
-                rm = next(x for x in dst.plan.messages if x.axis == axis and x.side == 1 - m.side)
-                _box(dst.sub.grid, rm.recv_box).copy_(payload)
-    torch.cuda.synchronize()
+    rts = halo.run_distributed_inprocess(dc)
+    for rt in rts:
+        assert rt.timings["compute_s"] > 0 and rt.timings["mlups"] > 0
     return halo.assemble_global(rts)
 
 
@@ -61,6 +38,9 @@ def _emulate(dc):
     ((1, 1, 2), (130, 70, 40), 4, "two_grid", 2, 0.5),
     ((1, 1, 2), (40, 40, 40), 4, "compressed", 2, None),
     ((2, 2, 1), (40, 40, 40), 2, "two_grid", 2, None),
+    ((2, 1, 1), (48, 20, 20), 4, "two_grid", 2, 1.0),
+    ((2, 2, 2), (24, 24, 24), 2, "two_grid", 3, None),
+    ((2, 1, 2), (32, 16, 32), 2, "compressed", 2, None),
 ])
 def test_zslab_gpu_equals_oracle(topo, gd, h, mode, cycles, ring, golden):
     cfg = sp.PipelineConfig(spec=sp.BlockSpec(8, 8, 8), t=h, grid_mode=mode)

@@ -237,3 +237,31 @@ def test_large_config_c4_single_gpu(golden):
     cfg = sp.PipelineConfig(spec=sp.BlockSpec(1024, 32, 32), t=4)
     st = sp.run_pipelined((a, a.copy()), cfg, 10)
     assert st.result.checksum() == c["digest"]
+
+
+@pytest.mark.slow
+def test_large_config_c5_single_gpu_window_anchors():
+    """BASELINE configs[4] on one B200: 2048^3 global (two 2050^3 grids =
+    137.8 GB of HBM), U[0,1) seed 42, ring 0.0, 32 sweeps at t=4.  Beyond
+    the CPU oracle's reach, so boxes at the faces, an edge, a corner and the
+    centre are checked with the light-cone window oracle."""
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
+    free, _ = torch.cuda.mem_get_info()
+    if free < 140e9:
+        pytest.skip(f"needs 140 GB of free HBM, {free / 1e9:.0f} GB free")
+    n = 2048
+    a = sp.create_grid(n, n, n, init="random", seed=42)
+    b = a.copy()
+    cfg = sp.PipelineConfig(spec=sp.BlockSpec(n, 32, 32), t=4)
+    st = sp.run_pipelined((a, b), cfg, 8)
+    res = st.result
+    boxes = (((0, 24), (1000, 1024), (2030, 2048)), ((1020, 1044), (2040, 2048), (0, 16)),
+             ((2032, 2048), (0, 16), (1016, 1040)), ((1010, 1030), (1010, 1030), (1010, 1030)))
+    for box in boxes:
+        exp = oracle.window_oracle((n, n, n), 42, box, 32)
+        (xl, xh), (yl, yh), (zl, zh) = box
+        assert_bitwise(res.interior_view()[zl:zh, yl:yh, xl:xh].cpu().numpy(), exp)
+    del a, b, res, st
+    torch.cuda.empty_cache()
