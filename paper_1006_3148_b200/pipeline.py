@@ -256,20 +256,31 @@ class PipelineEngine:
         return {u: [tuple(self.live_bounds(ax, u)) for ax in range(3)] for u in range(1, h + 1)}
 
     def _fusable(self, lives, h) -> bool:
-        """Fusing levels is exact when x/y are the full interior at every
-        level and every z live range is covered by the previous level's range
-        grown by one (or touches a ring)."""
-        nx, ny, nz = self.dims
+        """Fusing levels is exact when each level's live range is the previous
+        level's range shrunk by at least one cell per side, or keeps touching
+        the ring on that side: every live cell of the last level then depends
+        only on live cells of the levels before it, which the fused kernels
+        compute from the same level-0 data in the same order.  The kernels
+        store z only inside the last level's live range but whole x/y rows, so
+        an x/y side may shrink only where a neighbour owns it (the distributed
+        live bounds of sp/halo.py:278-289): those cells are ghosts that the
+        halo exchange overwrites.  Physical x/y sides must stay full."""
+        dims = self.dims
+        phys = self.physical_sides
         for u in range(1, h + 1):
-            (xl, xh), (yl, yh), (zl, zh) = lives[u]
-            if (xl, xh) != (0, nx) or (yl, yh) != (0, ny):
-                return False
-            if u >= 2:
-                pl, ph = lives[u - 1][2]
-                if not ((zl - 1 >= pl) or (zl == 0 and pl == 0)):
-                    return False
-                if not ((zh + 1 <= ph) or (zh == nz and ph == nz)):
-                    return False
+            for ax in range(3):
+                lo, hi = lives[u][ax]
+                if ax < 2:
+                    if phys[ax][0] and lo != 0:
+                        return False
+                    if phys[ax][1] and hi != dims[ax]:
+                        return False
+                if u >= 2:
+                    plo, phi = lives[u - 1][ax]
+                    if not ((lo - 1 >= plo) or (lo == 0 and plo == 0)):
+                        return False
+                    if not ((hi + 1 <= phi) or (hi == dims[ax] and phi == dims[ax])):
+                        return False
         return True
 
     def _check_rings_equal(self) -> bool:

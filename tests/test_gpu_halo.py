@@ -76,3 +76,15 @@ def test_c4_weak_scaling_p2_window_oracle():
         exp = oracle.window_oracle(gd, 42, box, 40, ring=1.0)
         (xl, xh), (yl, yh), (zl, zh) = box
         assert_bitwise(g.interior_view()[zl:zh, yl:yh, xl:xh].cpu().numpy(), exp)
+
+
+@pytest.mark.parametrize("topo", [(2, 1, 1), (2, 2, 1), (2, 2, 2), (1, 1, 2)])
+def test_general_topologies_take_the_fused_path(topo):
+    """Neighbour-owned x/y sides shrink like z: every rank's pass runs the
+    fused kernels, not the per-level windows."""
+    cfg = sp.PipelineConfig(spec=sp.BlockSpec(8, 8, 8), t=4)
+    subs = halo.decompose_domain((32, 32, 32), halo.RankTopology(*topo), halo.HaloSpec(4))
+    for s in subs:
+        rt = halo.RankRuntime(s, cfg, None)
+        assert rt.engine._fusable(rt.engine._lives(4), 4)
+        assert rt.engine.run_pass(1).kernel_launches == 1

@@ -105,6 +105,7 @@ def test_fusable_rule():
     sp/halo.py:278-289 qualify, arbitrary windows do not."""
     eng = PipelineEngine.__new__(PipelineEngine)
     eng.dims = (10, 10, 20)
+    eng.physical_sides = {ax: (True, True) for ax in range(3)}
     full = {u: [(0, 10), (0, 10), (0, 20)] for u in range(1, 5)}
     assert eng._fusable(full, 4)
     shrink = {u: [(0, 10), (0, 10), (u, 20 - u)] for u in range(1, 5)}
@@ -113,3 +114,9 @@ def test_fusable_rule():
     assert not eng._fusable(flat_inner, 4)
     xwin = {u: [(1, 9), (0, 10), (0, 20)] for u in range(1, 5)}
     assert not eng._fusable(xwin, 4)
+    # x/y sides owned by a neighbour may shrink (ghost cells); physical may not
+    xshrink = {u: [(u, 10 - u), (0, 10 - u), (0, 20)] for u in range(1, 5)}
+    assert not eng._fusable(xshrink, 4)
+    eng.physical_sides = {0: (False, False), 1: (True, False), 2: (True, True)}
+    assert eng._fusable(xshrink, 4)
+    assert not eng._fusable({u: [(1, 9), (0, 10 - u), (0, 20)] for u in range(1, 5)}, 4)
