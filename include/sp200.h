@@ -101,6 +101,17 @@ int sp_copy_ring(const double *a, double *b, int64_t ex, int64_t ey, int64_t ez,
                  int64_t nx, int64_t ny, int64_t nz, int64_t off, void *stream);
 
 /*
+ * *equal = 1 when the 1-cell shells (faces, edges, corners) of a and b at frame
+ * `off` hold equal values, else 0 — the precondition under which two-grid
+ * passes may fuse levels (the reference reads the ring of the grid each
+ * level alternates to, sp/pipeline.py:301-323).  Synchronises `stream` only:
+ * the verdict is written into host-mapped memory, so it does not wait behind
+ * bulk transfers queued on the copy engines by other streams.
+ */
+int sp_rings_equal(const double *a, const double *b, int64_t ex, int64_t ey, int64_t ez,
+                   int64_t nx, int64_t ny, int64_t nz, int64_t off, int *equal, void *stream);
+
+/*
  * Write Dirichlet faces at frame `off` (PipelineEngine._write_full_ring,
  * sp/pipeline.py:427-447; write_ring_strips, sp/kernel.py:61-82).  faces[0..5]
  * are device arrays in the layout of Grid3.boundary_faces (sp/grid.py:94-107):

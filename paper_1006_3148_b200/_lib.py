@@ -25,7 +25,7 @@ SP_MAX_FUSED = 4
 EXPORTS = (
     "sp_version", "sp_last_error", "sp_launch_count", "sp_fill_seeded",
     "sp_fill_constant", "sp_sweep", "sp_apply_window", "sp_window_gather",
-    "sp_copy_ring", "sp_write_faces", "sp_temporal", "sp_compressed_workspace",
+    "sp_copy_ring", "sp_rings_equal", "sp_write_faces", "sp_temporal", "sp_compressed_workspace",
     "sp_compressed", "sp_set_tuning", "sp_tma_eligible",
 )
 
@@ -51,6 +51,7 @@ def _declare(L):
                             i32),
         "sp_window_gather": ([dp, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64, dp, vp], i32),
         "sp_copy_ring": ([dp, dp, i64, i64, i64, i64, i64, i64, i64, vp], i32),
+        "sp_rings_equal": ([dp, dp, i64, i64, i64, i64, i64, i64, i64, ctypes.POINTER(i32), vp], i32),
         "sp_write_faces": ([dp, i64, i64, i64, i64, i64, i64, i64, ctypes.POINTER(dp), i32, vp], i32),
         "sp_temporal": ([dp, dp, i64, i64, i64, i64, i64, i64, i64, i32, i64, i64, vp], i32),
         "sp_compressed_workspace": ([i64, i64, i64, i32], i64),

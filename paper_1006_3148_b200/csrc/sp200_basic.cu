@@ -2,6 +2,7 @@
 //
 // These are the small / general-shape kernels.  The bandwidth-critical sweep
 // and the temporally blocked passes live in sp200_temporal.cu.
+#include <mutex>
 #include <stdarg.h>
 #include <stdio.h>
 #include <string.h>
@@ -166,35 +167,56 @@ __global__ void k_unstage(const double *scratch, double *dst, int64_t ex, int64_
 // one coordinate on the ring.  Enumerated as: two full z planes, then the two
 // y rows of every interior z plane, then the two x columns of the remaining
 // (interior z, interior y) rows.
+__device__ __forceinline__ int64_t shell_index(int64_t idx, int64_t ex, int64_t ey, int64_t nx,
+                                               int64_t ny, int64_t nz, int64_t off) {
+    const int64_t PX = nx + 2, PY = ny + 2;
+    const int64_t nzf = 2 * PX * PY, nyf = 2 * nz * PX;
+    int64_t x, y, z;
+    if (idx < nzf) {
+        int64_t f = idx / (PX * PY), r = idx % (PX * PY);
+        z = f ? off + nz : off - 1;
+        y = off - 1 + r / PX;
+        x = off - 1 + r % PX;
+    } else if (idx < nzf + nyf) {
+        int64_t q = idx - nzf;
+        int64_t f = q / (nz * PX), r = q % (nz * PX);
+        z = off + r / PX;
+        y = f ? off + ny : off - 1;
+        x = off - 1 + r % PX;
+    } else {
+        int64_t q = idx - nzf - nyf;
+        int64_t f = q / (nz * ny), r = q % (nz * ny);
+        z = off + r / ny;
+        y = off + r % ny;
+        x = f ? off + nx : off - 1;
+    }
+    return (z * ey + y) * ex + x;
+}
+
 __global__ void k_copy_ring(const double *a, double *b, int64_t ex, int64_t ey, int64_t nx,
                             int64_t ny, int64_t nz, int64_t off) {
-    const int64_t PX = nx + 2, PY = ny + 2;
-    const int64_t nzf = 2 * PX * PY, nyf = 2 * nz * PX, nxf = 2 * nz * ny;
-    const int64_t total = nzf + nyf + nxf;
+    const int64_t total = 2 * (nx + 2) * (ny + 2) + 2 * nz * (nx + 2) + 2 * nz * ny;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
-        int64_t x, y, z;
-        if (idx < nzf) {
-            int64_t f = idx / (PX * PY), r = idx % (PX * PY);
-            z = f ? off + nz : off - 1;
-            y = off - 1 + r / PX;
-            x = off - 1 + r % PX;
-        } else if (idx < nzf + nyf) {
-            int64_t q = idx - nzf;
-            int64_t f = q / (nz * PX), r = q % (nz * PX);
-            z = off + r / PX;
-            y = f ? off + ny : off - 1;
-            x = off - 1 + r % PX;
-        } else {
-            int64_t q = idx - nzf - nyf;
-            int64_t f = q / (nz * ny), r = q % (nz * ny);
-            z = off + r / ny;
-            y = off + r % ny;
-            x = f ? off + nx : off - 1;
-        }
-        int64_t p = (z * ey + y) * ex + x;
+        const int64_t p = shell_index(idx, ex, ey, nx, ny, nz, off);
         b[p] = a[p];
     }
+}
+
+// Ring equality (the precondition of fused two-grid passes).  The verdict is
+// written straight into host-mapped memory, so reading it waits only for
+// this stream, never behind bulk copies queued on the copy engines.
+__global__ void k_rings_equal(const double *a, const double *b, int64_t ex, int64_t ey,
+                              int64_t nx, int64_t ny, int64_t nz, int64_t off,
+                              volatile int *verdict) {
+    const int64_t total = 2 * (nx + 2) * (ny + 2) + 2 * nz * (nx + 2) + 2 * nz * ny;
+    bool same = true;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = shell_index(idx, ex, ey, nx, ny, nz, off);
+        same = same && (a[p] == b[p]);
+    }
+    if (__any_sync(0xffffffffu, !same) && (threadIdx.x & 31) == 0) *verdict = 0;
 }
 
 struct FaceArgs {
@@ -397,6 +419,36 @@ int sp_copy_ring(const double *a, double *b, int64_t ex, int64_t ey, int64_t ez,
                                                                       off);
     count_launch();
     return check_launch("sp_copy_ring");
+}
+
+int sp_rings_equal(const double *a, const double *b, int64_t ex, int64_t ey, int64_t ez,
+                   int64_t nx, int64_t ny, int64_t nz, int64_t off, int *equal, void *stream) {
+    if (!a || !b || !equal) return set_error(SP_EINVAL, "null argument");
+    int rc = check_geom(ex, ey, ez, nx, ny, nz, off);
+    if (rc) return rc;
+    static std::mutex mu;
+    static int *host_flag = nullptr, *dev_flag = nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!host_flag) {
+        if (cudaHostAlloc(reinterpret_cast<void **>(&host_flag), sizeof(int), cudaHostAllocMapped) !=
+                cudaSuccess ||
+            cudaHostGetDevicePointer(reinterpret_cast<void **>(&dev_flag), host_flag, 0) !=
+                cudaSuccess) {
+            host_flag = nullptr;
+            return set_error(SP_ECUDA, "mapped host flag: %s", cudaGetErrorString(cudaGetLastError()));
+        }
+    }
+    *reinterpret_cast<volatile int *>(host_flag) = 1;
+    int64_t total = 2 * (nx + 2) * (ny + 2) + 2 * nz * (nx + 2) + 2 * nz * ny;
+    k_rings_equal<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(a, b, ex, ey, nx, ny, nz,
+                                                                        off, dev_flag);
+    count_launch();
+    rc = check_launch("sp_rings_equal");
+    if (rc) return rc;
+    if (cudaStreamSynchronize(as_stream(stream)) != cudaSuccess)
+        return set_error(SP_ECUDA, "sp_rings_equal: %s", cudaGetErrorString(cudaGetLastError()));
+    *equal = *reinterpret_cast<volatile int *>(host_flag);
+    return SP_OK;
 }
 
 int sp_write_faces(double *data, int64_t ex, int64_t ey, int64_t ez, int64_t nx, int64_t ny,

@@ -109,6 +109,20 @@ def copy_ring(a: Grid3, b: Grid3) -> None:
                                         a.nz, a.offset, _stream()), "copy_ring")
 
 
+def rings_equal(a: Grid3, b: Grid3) -> bool:
+    """True when A and B hold equal one-cell shells (faces, edges, corners)
+    at their frame — the precondition for fusing two-grid levels.  Waits only
+    for the current stream (the verdict comes back through host-mapped
+    memory, not a copy engine)."""
+    if a.data.shape != b.data.shape or a.offset != b.offset:
+        return False
+    ex, ey, ez = a.extents
+    eq = ctypes.c_int(0)
+    _lib.check(_lib.load().sp_rings_equal(_ptr(a.data), _ptr(b.data), ex, ey, ez, a.nx, a.ny,
+                                          a.nz, a.offset, ctypes.byref(eq), _stream()), "rings_equal")
+    return bool(eq.value)
+
+
 def reference_sweep(a: Grid3, b: Grid3) -> None:
     """One plain Jacobi sweep: B.interior = stencil(A), B.ring = A.ring
     (sp/kernel.py:99-111) — K1, the streaming sweep with the fused ring copy."""

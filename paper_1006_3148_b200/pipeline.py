@@ -31,7 +31,7 @@ import torch
 
 from . import _lib
 from .grid import BlockSpec, Grid3, decompose_blocks
-from .kernel import (apply_window, compressed_pass, compressed_workspace, fused_sweeps,
+from .kernel import (apply_window, compressed_pass, compressed_workspace, fused_sweeps, rings_equal,
                      write_faces, write_ring_strips)
 
 MAX_FUSED = _lib.SP_MAX_FUSED
@@ -286,19 +286,7 @@ class PipelineEngine:
     def _check_rings_equal(self) -> bool:
         if self._rings_equal is None:
             a, b = self.grids
-            o = a.offset
-            nx, ny, nz = self.dims
-            da, db = a.data, b.data
-            sl = (slice(o - 1, o + nz + 1), slice(o - 1, o + ny + 1), slice(o - 1, o + nx + 1))
-            eq = True
-            for axis in range(3):
-                for face in (o - 1, o + (nz, ny, nx)[axis]):
-                    idx = list(sl)
-                    idx[axis] = face
-                    idx = tuple(idx)
-                    if not torch.equal(da[idx], db[idx]):
-                        eq = False
-            self._rings_equal = eq
+            self._rings_equal = rings_equal(a, b)
         return self._rings_equal
 
     # -- passes ---------------------------------------------------------------
@@ -435,8 +423,10 @@ def team_sweep(grids, cfg: PipelineConfig, direction: int = 1) -> RunStats:
 
 def run_pipelined(grids, cfg: PipelineConfig, total_passes: int) -> RunStats:
     """Alternate forward/backward passes (sp/pipeline.py:527-548).  Compressed
-    mode needs an even number of passes and pad >= h.  Synchronises the device
-    at the end so wall_seconds / mlups cover the GPU work."""
+    mode needs an even number of passes and pad >= h.  Synchronises the
+    current stream at both ends so wall_seconds / mlups cover the GPU work;
+    work on other streams (e.g. host transfers of the next input) keeps
+    running."""
     engine = PipelineEngine(cfg, grids)
     if cfg.grid_mode == "compressed":
         if total_passes % 2 != 0:
@@ -445,12 +435,13 @@ def run_pipelined(grids, cfg: PipelineConfig, total_passes: int) -> RunStats:
             raise ValueError(
                 f"compressed mode needs pad >= h ({engine.grids[0].pad} < {cfg.h})")
     stats = RunStats()
-    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    stream.synchronize()
     t0 = time.perf_counter()
     for p in range(total_passes):
         direction = 1 if p % 2 == 0 else -1
         stats.merge_pass(engine.run_pass(direction))
-    torch.cuda.synchronize()
+    stream.synchronize()
     stats.wall_seconds = time.perf_counter() - t0
     nx, ny, nz = engine.dims
     stats.updates_total = nx * ny * nz * cfg.h * total_passes

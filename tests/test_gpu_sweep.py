@@ -220,3 +220,21 @@ def test_no_cpu_fallback_without_library(monkeypatch):
     monkeypatch.setattr(_lib, "_lib", None)
     with pytest.raises(ImportError):
         _lib.load("/nonexistent/libsp200.so")
+
+
+def test_rings_equal_sees_faces_edges_and_corners():
+    a = sp.create_grid(9, 7, 5, pad=1, init="random", seed=5, ring=0.25)
+    b = a.copy()
+    assert sp.rings_equal(a, b)
+    o = a.offset
+    for cell in ((o - 1, o + 2, o + 3), (o + 5, o - 1, o - 1), (o - 1, o - 1, o + 9),
+                 (o + 2, o + 3, o + 9)):
+        c = a.copy()
+        c.data[cell] += 1.0
+        assert not sp.rings_equal(a, c), cell
+    c = a.copy()
+    c.data[o + 2, o + 3, o + 4] += 1.0  # interior cells do not count
+    assert sp.rings_equal(a, c)
+    d = sp.create_grid(9, 7, 5, pad=1, init="random", seed=5, ring=0.0)
+    sp.copy_ring(a, d)
+    assert sp.rings_equal(a, d)
