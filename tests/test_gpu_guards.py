@@ -1,0 +1,88 @@
+"""GPU: out-of-bounds write detection without a sanitizer.  Every grid and
+the K3 stash live in the middle of a larger buffer filled with a canary
+pattern; after K1, K2 (all depths, both loaders, z-chunks, live ranges),
+K3 (both directions, depths 1-4), the window seam, faces and ring kernels,
+the guard regions must be untouched and the results must still match the
+oracle bit for bit."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import assert_bitwise
+
+pytestmark = pytest.mark.gpu
+
+sp = pytest.importorskip("paper_1006_3148_b200")
+from paper_1006_3148_b200.kernel import compressed_pass  # noqa: E402
+
+GUARD = 1 << 16  # doubles on each side (512 KB)
+CANARY = -7.25e300
+
+
+def guarded(shape):
+    n = int(np.prod(shape))
+    buf = torch.full((n + 2 * GUARD,), CANARY, dtype=torch.float64, device="cuda")
+    return buf, buf[GUARD:GUARD + n].view(shape)
+
+
+def intact(buf, n):
+    return bool(torch.all(buf[:GUARD] == CANARY)) and bool(torch.all(buf[GUARD + n:] == CANARY))
+
+
+def guarded_grid(nx, ny, nz, pad=0, **kw):
+    src = sp.create_grid(nx, ny, nz, pad=pad, **kw)
+    buf, view = guarded(tuple(src.data.shape))
+    view.copy_(src.data)
+    g = sp.Grid3(nx, ny, nz, pad, data=view)
+    g.boundary_faces = src.boundary_faces
+    return buf, g
+
+
+@pytest.mark.parametrize("dims", [(70, 37, 21), (64, 32, 16), (5, 3, 2), (130, 66, 9)])
+def test_two_grid_kernels_stay_in_bounds(dims):
+    L = sp._lib.load()
+    for force in (0, 1):
+        L.sp_set_tuning(1, force)
+        try:
+            ba, a = guarded_grid(*dims, init="random", seed=1, ring=0.5)
+            bb, b = guarded_grid(*dims, init="random", seed=1, ring=0.5)
+            d = oracle.make_storage(*dims, init="random", seed=1, ring=0.5)
+            sp.reference_sweep(a, b)
+            levels, cur, oth = 1, b, a
+            for t in (2, 3, 4):
+                sp.fused_sweeps(cur, oth, t)
+                levels += t
+                cur, oth = oth, cur
+            n = a.data.numel()
+            assert intact(ba, n) and intact(bb, n)
+            exp = oracle.interior(oracle.sweeps(d, dims, levels), *dims)
+            assert_bitwise(cur.interior_numpy(), exp)
+            sp.fused_sweeps(a, b, 4, 1, max(2, dims[2] - 1))
+            sp.apply_window(a.data, a.data, ((0, dims[0]), (0, dims[1]), (0, dims[2])), a.offset, a.offset)
+            sp.copy_ring(a, b)
+            assert sp.rings_equal(a, b)
+            assert intact(ba, n) and intact(bb, n)
+        finally:
+            L.sp_set_tuning(1, 0)
+
+
+@pytest.mark.parametrize("t,dims", [(4, (66, 35, 24)), (3, (61, 29, 19)), (2, (130, 70, 12)),
+                                    (1, (20, 9, 7))])
+def test_compressed_kernels_stay_in_bounds(t, dims):
+    bg, g = guarded_grid(*dims, pad=t, init="random", seed=3, lo=-1.0, hi=1.0)
+    n = g.data.numel()
+    nbytes = int(sp._lib.load().sp_compressed_workspace(dims[0], dims[1], dims[2], t))
+    wbuf = torch.full((max(nbytes, 256) // 8 + 2 * GUARD + 1,), CANARY, dtype=torch.float64, device="cuda")
+    ws = wbuf[GUARD:GUARD + max(nbytes, 256) // 8 + 1].view(torch.uint8)
+    d = oracle.make_storage(*dims, pad=t, init="random", seed=3, lo=-1.0, hi=1.0)
+    for p, direction in enumerate((1, -1, 1, -1)):
+        compressed_pass(g, t, direction, g.alignment, ws)
+        g.alignment += t * direction
+    assert intact(bg, n)
+    assert bool(torch.all(wbuf[:GUARD] == CANARY))
+    assert bool(torch.all(wbuf[GUARD + max(nbytes, 256) // 8 + 1:] == CANARY))
+    exp = oracle.interior(oracle.sweeps(oracle.make_storage(*dims, init="random", seed=3, lo=-1.0, hi=1.0),
+                                        dims, 4 * t), *dims)
+    assert_bitwise(g.interior_numpy(), exp)
