@@ -294,9 +294,15 @@ static int launch_cfg(const double *src, double *dst, int64_t ex, int64_t ey, in
     const int64_t slots = (int64_t)sm_count() * occ;
     int64_t zc = tuning().zchunk;
     if (zc <= 0) {
+        // Chunks of 24-40 planes measured fastest on every size (512^3: 379
+        // vs 355 GLUP/s for whole columns, 2048^3: 357 vs 279): concurrently
+        // running CTAs re-align in z at every chunk, so their streams keep
+        // hitting the same DRAM pages instead of drifting apart.
+        const int64_t lmin = std::min<int64_t>(depth, 24), lmax = 40;
         double best = 1e300;
-        for (int64_t c = 1; c <= 256 && c <= depth; ++c) {
+        for (int64_t c = 1; c <= 4096 && c <= depth; ++c) {
             int64_t len = (depth + c - 1) / c;
+            if (len > lmax || len < lmin) continue;
             int64_t units = p.ntiles * ((depth + len - 1) / len);
             double waves = (double)((units + slots - 1) / slots);
             // partial last wave still costs a whole wave; a short chunk pays the
