@@ -25,6 +25,8 @@
 //    cell per side per level; the stored tile is OX x (CY-2(T-1)).  Cells
 //    outside the interior (Dirichlet ring) keep their input value at every
 //    level.
+#include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -70,7 +72,10 @@ struct KCfg {
     static constexpr int OY = CY - 2 * (T - 1);
     static constexpr int NLEV = (T > 1) ? 2 * (T - 1) : 0;
     static constexpr int XBW = 2 * T + 2;        // K3 x-stash columns per tile (even)
-    static constexpr size_t SMEM = (size_t)(S + NLEV) * PLANE_AL * sizeof(double) + 8 * S + 16;
+    // mbarriers: S stage barriers, then (cluster launches) the halo-row
+    // barriers rx_lo[T-1][2] and rx_hi[T-1][2]
+    static constexpr int NBAR = S + 4 * (T > 1 ? T - 1 : 0);
+    static constexpr size_t SMEM = (size_t)(S + NLEV) * PLANE_AL * sizeof(double) + 8 * NBAR + 16;
     // CTAs per SM the shared memory allows (1 KB per CTA is reserved by the
     // runtime); the register budget follows through __launch_bounds__
     static constexpr int MINB = (2 * (SMEM + 1024) <= 232448) ? 2 : 1;
@@ -107,12 +112,23 @@ __device__ __forceinline__ void stg2_stream(double *p, double a, double b) {
 // written in place.  No inter-CTA ordering is needed, so K3 runs on K2's
 // tile-fastest schedule (the reference needs the same order-dependence only
 // because its blocks run in lexicographic order, sp/grid.py:195-204).
-template <int T, int CY, int R, int S, bool TMA, bool COMP>
+//
+// CL > 1 (two-grid only): a thread-block cluster of CL CTAs stacked in y
+// shares one overlapped tile of 64 x CL*CY region rows, so the ghost zone is
+// paid once per cluster instead of once per CTA.  Each step the boundary
+// warps push their published row of every level 1..T-1 into the adjacent
+// CTA's halo row with st.async (DSMEM), completing a per-(level, parity)
+// mbarrier there; only the receiving boundary warp waits, one step later.
+template <int T, int CY, int R, int S, bool TMA, bool COMP, int CL>
 __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB)
     k_temporal(const TParams p, const __grid_constant__ CUtensorMap tmap) {
     using C = KCfg<T, CY, R, S>;
     constexpr int SPX = C::SPX, C0 = C::C0, PLANE = C::PLANE, PLANE_AL = C::PLANE_AL,
                   NT = C::NT;
+    constexpr int NW = NT / 32;
+    // stored rows of the (cluster) tile
+    constexpr int OYc = CL * CY - 2 * (T - 1);
+    static_assert(CL == 1 || (!COMP && T > 1), "clusters: two-grid fused passes only");
 
     extern __shared__ __align__(128) double sm[];
     double *stage = sm;
@@ -127,14 +143,34 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     const int i0 = 2 * lane;   // region column of this lane's first cell
     const int j0 = warp * R;   // first region row
 
-    if constexpr (TMA) {
+    const int rank = (CL > 1) ? (int)cluster_ctarank() : 0;
+    [[maybe_unused]] uint64_t *rx_lo = bar + S, *rx_hi = bar + S + 2 * (T - 1);
+    // halo role of this warp: 1 = first warp of a CTA below another (sends
+    // its first row up, receives rx_lo), 2 = last warp of a CTA above another
+    [[maybe_unused]] int role = 0;
+    [[maybe_unused]] uint32_t peer_base = 0;  // shared::cluster address of the peer's smem
+    if constexpr (CL > 1) {
+        if (warp == 0 && rank > 0) role = 1;
+        else if (warp == NW - 1 && rank < CL - 1) role = 2;
+        if (role) peer_base = mapa_u32(smem_u32(sm), (uint32_t)(role == 1 ? rank - 1 : rank + 1));
+    }
+    if constexpr (TMA || CL > 1) {
         if (tid == 0) {
-            tma_prefetch_desc(&tmap);
+            if constexpr (TMA) tma_prefetch_desc(&tmap);
 #pragma unroll
             for (int si = 0; si < S; ++si) mbar_init(&bar[si], 1);
+            if constexpr (CL > 1) {
+                // arm phase 0 of every halo barrier: 64 doubles per row
+#pragma unroll
+                for (int i = 0; i < 4 * (T - 1); ++i) {
+                    mbar_init(&bar[S + i], 1);
+                    mbar_arrive_expect_tx(&bar[S + i], 64 * 8);
+                }
+            }
             fence_mbar_init();
         }
-        __syncthreads();
+        if constexpr (CL > 1) cluster_sync_all();  // peers' barriers exist before any st.async
+        else __syncthreads();
     }
 
     LState<T, R> st;
@@ -155,13 +191,15 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     // one (tile, z-chunk) unit per CTA, tile-fastest so that concurrently
     // running CTAs cover neighbouring tiles at the same z range and the
     // overlapped halo reads hit L2
-    const int tile = p.tile_base + (int)(blockIdx.x % p.tile_count);
-    const int chunk = (int)(blockIdx.x / p.tile_count);
+    const int cid = (int)(blockIdx.x / CL);
+    const int tile = p.tile_base + cid % p.tile_count;
+    const int chunk = cid / p.tile_count;
     const int z0 = p.zlo + chunk * p.zc;
     const int z1 = min(z0 + p.zc, p.zhi);
     const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
-    const int x0 = tx * p.ox, y0 = ty * C::OY;
-    const int rx0 = x0 - p.ex0, ry0 = y0 - (T - 1);  // logical coords of region (0, 0)
+    const int x0 = tx * p.ox, y0 = ty * OYc;
+    // logical coords of this CTA's region (0, 0)
+    const int rx0 = x0 - p.ex0, ry0 = y0 - (T - 1) + rank * CY;
 
     // Dirichlet ring cells keep their value at every level; cells beyond the
     // ring are computed but never read by a kept cell, so only the ring
@@ -182,8 +220,8 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     bool y_out[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        const int jr = j0 + r, y = ry0 + jr;
-        y_out[r] = (jr >= T - 1) && (jr < T - 1 + C::OY) && (y < p.ny);
+        const int jr = rank * CY + j0 + r, y = ry0 + j0 + r;  // jr: row of the cluster region
+        y_out[r] = (jr >= T - 1) && (jr < T - 1 + OYc) && (y < p.ny);
     }
     // warps without ring cells skip the select
     const bool wint = !__any_sync(0xffffffffu, ringb != 0u);
@@ -208,12 +246,12 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     int ky0;
     {
         const int yo = ry0 + j0 - y0;
-        ky0 = fwd ? (ty - 1) * 2 * T + yo : ty * 2 * T + yo - (C::OY - 2 * T);
+        ky0 = fwd ? (ty - 1) * 2 * T + yo : ty * 2 * T + yo - (OYc - 2 * T);
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int yo = ry0 + j0 + r - y0;
-        yb[r] = COMP && (fwd ? (ty > 0 && yo < 2 * T) : (ty < p.tiles_y - 1 && yo >= C::OY - 2 * T));
+        yb[r] = COMP && (fwd ? (ty > 0 && yo < 2 * T) : (ty < p.tiles_y - 1 && yo >= OYc - 2 * T));
     }
     const int nchunks = (p.zhi - p.zlo + p.zc - 1) / p.zc;
     const bool zband_chunk = COMP && (fwd ? chunk > 0 : chunk < nchunks - 1);
@@ -289,6 +327,15 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
                     st.W0[Q][r][1] = a.y;
                 }
             }
+            if constexpr (CL > 1) {
+                // level u-1's boundary row of the adjacent CTA (sent at step s-1)
+                if (u > 1 && s > 0 && role && !(SP200_PROFILE_KNOBS && (p.debug & 8))) {
+                    uint64_t *hb = (role == 1 ? rx_lo : rx_hi) + (u - 2) * 2 + (Q ^ 1);
+                    mbar_wait(hb, ((uint32_t)(s - 1) >> 1) & 1u);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_expect_tx(hb, 64 * 8);  // arm the next phase
+                }
+            }
             const double2 cm = lds2(B + j0 * SPX + C0 + i0);
             const double2 cp = lds2(B + (j0 + R + 1) * SPX + C0 + i0);
             double *pub = lev + ((u - 1) * 2 + Q) * PLANE_AL;
@@ -318,7 +365,8 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 if (u == 1) {
-                    // level 0 lives in the stage: outer x-neighbours straight from smem
+                    // level 0 lives in the stage: outer x-neighbours straight from
+                    // smem (shuffles here measured 636 vs 771 GLUP/s at T=4)
                     xl[r] = B[(j0 + r + 1) * SPX + C0 + i0 - 1];
                     xr[r] = B[(j0 + r + 1) * SPX + C0 + i0 + 2];
                 } else {
@@ -365,6 +413,19 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
             for (int r = 0; r < R; ++r) {
                 if (u < T) {
                     if (r == 0 || r == R - 1) sts2(pub + (j0 + r + 1) * SPX + C0 + i0, v[r][0], v[r][1]);
+                    if constexpr (CL > 1) {
+                        // push the CTA's first (role 1) / last (role 2) region
+                        // row into the adjacent CTA's halo row; the peer's
+                        // shared memory has the same layout
+                        if (s + 1 < nsteps && ((role == 1 && r == 0) || (role == 2 && r == R - 1))) {
+                            const uint32_t prow = (uint32_t)((pub - sm) + C0) * 8u +
+                                                  (role == 1 ? (uint32_t)((CY + 1) * SPX * 8) : 0u);
+                            const uint32_t pbar = (uint32_t)(reinterpret_cast<char *>(
+                                                      (role == 1 ? rx_hi : rx_lo) + (u - 1) * 2 + Q) -
+                                                  reinterpret_cast<char *>(sm));
+                            st_async_f64x2(peer_base + prow + lane * 16u, v[r][0], v[r][1], peer_base + pbar);
+                        }
+                    }
                 } else if (store_plane && y_out[r]) {
                     if constexpr (COMP) {
                         // band priority y, then z, then x (k_unstash_* skip
@@ -429,6 +490,8 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     if constexpr (!TMA) cp_async_wait<0>();
     gbase += (uint32_t)nload;
     }  // units
+    // no CTA leaves while a peer may still address its shared memory
+    if constexpr (CL > 1) cluster_sync_all();
 }
 
 struct UnstashArgs {
@@ -547,16 +610,41 @@ struct LaunchReq {
     cudaStream_t stream;
 };
 
-template <int T, int CY>
+template <int T, int CY, int CL = 1>
 static int tile_geometry(int64_t nx, int64_t ny, int64_t off, bool aligned, int *ox, int *ex0,
                          int *tiles_x, int *tiles_y) {
     using C = KCfg<T, CY, 4, 4>;
+    constexpr int OYc = CL * CY - 2 * (T - 1);
     const int par = aligned ? (int)((off - (T - 1)) & 1) : 0;
     *ox = C::CX - 2 * (T - 1) - 2 * par;
     *ex0 = (T - 1) + par;
     *tiles_x = (int)((nx + *ox - 1) / *ox);
-    *tiles_y = (int)((ny + C::OY - 1) / C::OY);
+    *tiles_y = (int)((ny + OYc - 1) / OYc);
     return par;
+}
+
+// <<<>>> for CL == 1, cudaLaunchKernelEx with a (CL, 1, 1) cluster otherwise;
+// `units` counts tiles x chunks, CL CTAs each
+template <int CL, typename K>
+static void launch_units(K kern, int64_t units, int nt, size_t smem, cudaStream_t stream,
+                         const TParams &p, const CUtensorMap &tmap) {
+    if constexpr (CL == 1) {
+        kern<<<(unsigned)units, nt, smem, stream>>>(p, tmap);
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(units * CL), 1, 1);
+        cfg.blockDim = dim3(nt, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = CL;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, kern, p, tmap);
+    }
 }
 
 static int64_t pick_zchunk(int64_t depth, int64_t ntiles, int64_t slots, int T) {
@@ -601,10 +689,13 @@ static void comp_layout(int64_t nx, int64_t ny, int64_t depth, int64_t off, bool
     L->nz_stash = (L->nchunks - 1) * 2 * T * ny * ((nx + 2) & ~1);
 }
 
-template <int T, int CY, int R, int S>
+template <int T, int CY, int R, int S, int CL = 1>
 static int launch_cfg(const LaunchReq &q) {
     using C = KCfg<T, CY, R, S>;
     const bool comp = q.direction != 0;
+    if constexpr (CL > 1) {
+        if (comp) return launch_cfg<T, CY, R, S, 1>(q);  // K3 runs unclustered
+    }
     // Pair alignment: region column 0 must sit at an even storage x (16-byte
     // aligned pairs for LDS.128 / STG.128 and the TMA box origin).  Tiles
     // start at multiples of the (even) stored width, so the parity of the
@@ -615,7 +706,7 @@ static int launch_cfg(const LaunchReq &q) {
         (q.ex % 2 == 0);
     TParams p;
     int tiles_y;
-    tile_geometry<T, CY>(q.nx, q.ny, q.off, aligned, &p.ox, &p.ex0, &p.tiles_x, &tiles_y);
+    tile_geometry<T, CY, CL>(q.nx, q.ny, q.off, aligned, &p.ox, &p.ex0, &p.tiles_x, &tiles_y);
     const bool use_tma =
         aligned && !tuning().force_cpasync && tma_eligible(q.src, q.ex, q.ey) && encode_fn();
     p.src = q.src;
@@ -639,10 +730,15 @@ static int launch_cfg(const LaunchReq &q) {
     p.wx2 = p.hy2 = 0;
 
     void (*kern)(const TParams, const CUtensorMap);
-    if (comp)
-        kern = use_tma ? k_temporal<T, CY, R, S, true, true> : k_temporal<T, CY, R, S, false, true>;
-    else
-        kern = use_tma ? k_temporal<T, CY, R, S, true, false> : k_temporal<T, CY, R, S, false, false>;
+    if constexpr (CL > 1) {
+        kern = use_tma ? k_temporal<T, CY, R, S, true, false, CL>
+                       : k_temporal<T, CY, R, S, false, false, CL>;
+    } else if (comp) {
+        kern = use_tma ? k_temporal<T, CY, R, S, true, true, 1> : k_temporal<T, CY, R, S, false, true, 1>;
+    } else {
+        kern = use_tma ? k_temporal<T, CY, R, S, true, false, 1>
+                       : k_temporal<T, CY, R, S, false, false, 1>;
+    }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)C::SMEM);
     if (e != cudaSuccess)
@@ -652,7 +748,25 @@ static int launch_cfg(const LaunchReq &q) {
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::NT, C::SMEM);
     if (occ < 1) occ = 1;
-    const int64_t slots = (int64_t)sm_count() * occ;
+    // concurrently resident units (tiles x chunks), CL CTAs each
+    int64_t slots = (int64_t)sm_count() * occ / CL;
+    if constexpr (CL > 1) {
+        cudaLaunchConfig_t oc = {};
+        oc.gridDim = dim3((unsigned)(slots * CL), 1, 1);
+        oc.blockDim = dim3(C::NT, 1, 1);
+        oc.dynamicSmemBytes = C::SMEM;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = CL;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        oc.attrs = at;
+        oc.numAttrs = 1;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, kern, &oc) == cudaSuccess && ncl > 0) slots = ncl;
+        cudaGetLastError();
+        if (getenv("SP200_VERBOSE")) fprintf(stderr, "sp200: T=%d CL=%d max active clusters %d\n", T, CL, ncl);
+    }
     int64_t grid;
     CompLayout L;
     if (comp) {
@@ -675,7 +789,7 @@ static int launch_cfg(const LaunchReq &q) {
     }
     p.tile_base = 0;
     p.tile_count = p.ntiles;
-    if (grid > 0x7fffffff) return set_error(SP_EUNSUP, "grid too large");
+    if (grid * CL > 0x7fffffff) return set_error(SP_EUNSUP, "grid too large");
 
     CUtensorMap tmap;
     memset(&tmap, 0, sizeof(tmap));
@@ -701,7 +815,7 @@ static int launch_cfg(const LaunchReq &q) {
         a.tile_base = 0;
         a.tile_count = full;
         a.zc = (int)depth;
-        kern<<<(unsigned)full, C::NT, C::SMEM, q.stream>>>(a, tmap);
+        launch_units<CL>(kern, full, C::NT, C::SMEM, q.stream, a, tmap);
         count_launch();
         int rc = check_launch("k_temporal");
         if (rc || rem == 0) return rc;
@@ -711,11 +825,11 @@ static int launch_cfg(const LaunchReq &q) {
         const int64_t zcb = pick_zchunk(depth, rem, slots, T);
         b.zc = (int)zcb;
         const int64_t gb = (int64_t)rem * ((depth + zcb - 1) / zcb);
-        kern<<<(unsigned)gb, C::NT, C::SMEM, q.stream>>>(b, tmap);
+        launch_units<CL>(kern, gb, C::NT, C::SMEM, q.stream, b, tmap);
         count_launch();
         return check_launch("k_temporal");
     }
-    kern<<<(unsigned)grid, C::NT, C::SMEM, q.stream>>>(p, tmap);
+    launch_units<CL>(kern, grid, C::NT, C::SMEM, q.stream, p, tmap);
     count_launch();
     int rc = check_launch("k_temporal");
     if (rc || !comp) return rc;
@@ -760,6 +874,16 @@ static int launch_cfg(const LaunchReq &q) {
 }
 
 static int dispatch(int levels, const LaunchReq &q) {
+    if (q.direction != 0) {
+        // K3: the CY = 32 instances, the geometry compressed_workspace sizes
+        switch (levels) {
+        case 1: return launch_cfg<1, 32, 4, 4>(q);
+        case 2: return launch_cfg<2, 32, 4, 6>(q);
+        case 3: return launch_cfg<3, 32, 4, 5>(q);
+        case 4: return launch_cfg<4, 32, 4, 4>(q);
+        default: return set_error(SP_EUNSUP, "levels %d unsupported", levels);
+        }
+    }
     const int idx = (int)tuning().cfg_index[levels];
     switch (levels) {
     case 1: return launch_cfg<1, 32, 4, 4>(q);
@@ -768,21 +892,27 @@ static int dispatch(int levels, const LaunchReq &q) {
         case 1: return launch_cfg<2, 32, 4, 4>(q);
         case 2: return launch_cfg<2, 16, 2, 4>(q);
         case 3: return launch_cfg<2, 24, 2, 4>(q);
-        default: return launch_cfg<2, 32, 4, 6>(q);
+        case 4: return launch_cfg<2, 32, 4, 6, 2>(q);
+        case 5: return launch_cfg<2, 32, 4, 6>(q);
+        default: return launch_cfg<2, 48, 4, 4>(q);  // 12 warps: 644 vs 602 GLUP/s (CY=32)
         }
     case 3:
         switch (idx) {
         case 1: return launch_cfg<3, 32, 4, 3>(q);
         case 2: return launch_cfg<3, 16, 2, 4>(q);
         case 3: return launch_cfg<3, 24, 2, 4>(q);
-        default: return launch_cfg<3, 32, 4, 5>(q);
+        case 4: return launch_cfg<3, 32, 4, 5, 2>(q);
+        case 5: return launch_cfg<3, 32, 4, 5>(q);
+        default: return launch_cfg<3, 36, 3, 4>(q);  // 12 warps: 727 vs 701 GLUP/s (CY=32)
         }
     case 4:
         switch (idx) {
         case 1: return launch_cfg<4, 32, 4, 3>(q);
         case 2: return launch_cfg<4, 16, 2, 4>(q);
         case 3: return launch_cfg<4, 24, 2, 4>(q);
-        default: return launch_cfg<4, 32, 4, 4>(q);
+        case 4: return launch_cfg<4, 32, 4, 4, 2>(q);
+        case 5: return launch_cfg<4, 36, 3, 4>(q);
+        default: return launch_cfg<4, 32, 4, 4>(q);  // 8 warps x 254 registers
         }
     default:
         return set_error(SP_EUNSUP, "levels %d unsupported", levels);
