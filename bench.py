@@ -216,7 +216,7 @@ def run_ours(args):
     if slab:
         from paper_1006_3148_b200 import halo
         solver = halo.SlabSolver.weak(per_rank=(N_INT, N_INT, N_INT), seed=SEED, ring=0.0,
-                                      depth=args.t)
+                                      depth=args.t, transport=args.transport)
         lups_rank = N_INT ** 3 * SWEEPS
 
         def step(timer=None):
@@ -307,6 +307,30 @@ def run_ours(args):
             traffic = None
 
     extra = {}
+    # The fused pass is not HBM-bound: report the FP64 pipe it runs against.
+    # Peak = 64 FP64 lanes/clk/SM (tools/microbench.cu) x SMs x max SM clock;
+    # "useful" counts 6 flops per LUP, "executed" adds the overlapped-tile
+    # recompute of the K2 geometry (csrc/sp200_temporal.cu tile_geometry).
+    try:
+        props = torch.cuda.get_device_properties(local)
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f).get("sm_max_mhz", 1965.0))
+    except Exception:
+        mhz = 1965.0
+    fp64_peak = 64 * props.multi_processor_count * mhz * 1e6 / 1e12
+    if dom_depth > 1:
+        cy = {2: 48, 3: 36, 4: 32}.get(dom_depth, 32)
+        ox, oy = 64 - 2 * (dom_depth - 1), cy - 2 * (dom_depth - 1)
+        redundancy = (-(-N_INT // ox) * 64) * (-(-N_INT // oy) * cy) / N_INT ** 2
+    else:
+        redundancy = 1.0
+    useful = value / ws * 6 / 1e3
+    extra["compute_roofline"] = {
+        "bound": "fp64_pipe", "unit": "TFLOP/s (per GPU)", "peak": fp64_peak,
+        "achieved_useful": useful, "frac_useful": useful / fp64_peak,
+        "executed_lup_per_lup": redundancy, "frac_executed": useful * redundancy / fp64_peak,
+        "note": ("6 DADD/DMUL per LUP, no FMA (bit-exact order); ncu K2 T=4: "
+                 "sm__pipe_fp64_cycles_active 38%, issue active 40%, 8 warps/SM (profiles/r01_ncu_k2_t4.txt)")}
     if rank == 0 and not slab and not args.quick:
         # per-depth GLUP/s (t=1 is the plain sweep K1), 3 timed solves each
         per = {}
@@ -482,6 +506,7 @@ def run_ours(args):
                                     f"{args.t}-deep ghosts via NCCL, 100 sweeps"),
                        "fused_depth": args.t, "sweeps_per_step": SWEEPS,
                        "parallelism": f"z-slab x{ws}" if ws > 1 else "single GPU",
+                       "halo_transport": args.transport if slab else None,
                        "l2_flush": "not needed: 2.2 GB working set > 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -511,6 +536,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-sweeps-per-step", type=int, default=2)
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
+                    help="z-slab halo delivery for N>1: NCCL P2P, or the fused peer-memory stores")
     ap.add_argument("--slab", action="store_true",
                     help="use the distributed z-slab driver even on one GPU (path check)")
     args = ap.parse_args()

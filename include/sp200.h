@@ -156,11 +156,47 @@ int sp_compressed(double *data, int64_t ex, int64_t ey, int64_t ez,
                   int levels, int64_t zlo, int64_t zhi, void *workspace,
                   const double *const faces[6], int side_mask, void *stream);
 
+/*
+ * Fused pass with peer delivery (z-slab halo exchange over NVLink peer
+ * memory).  Same as sp_temporal, and every plane of [zlo, zhi) it stores is
+ * also stored into `mirror` — a neighbouring rank's grid with the same x/y
+ * storage extents, mapped with sp_ipc_open — at storage plane
+ * z + off + mirror_zshift (mirror_ez planes).  Replaces the post-pass send /
+ * receive of those planes (sp/halo.py:239-271 exchange_multilayer_halos,
+ * sp/transport.py:58-60 Endpoint.sendrecv) for the topology (1,1,P):
+ * the kernel writes the neighbour's ghost planes while it computes them.
+ */
+int sp_temporal_mirror(const double *src, double *dst, int64_t ex, int64_t ey, int64_t ez,
+                       int64_t nx, int64_t ny, int64_t nz, int64_t off, int levels,
+                       int64_t zlo, int64_t zhi, double *mirror, int64_t mirror_ez,
+                       int64_t mirror_zshift, void *stream);
+
+/*
+ * CUDA IPC for the peer mappings (the rendezvous of sp/transport.py:194-237,
+ * without a byte transport).  sp_ipc_handle writes the 64-byte handle of the
+ * allocation holding `ptr` and ptr's byte offset inside it; sp_ipc_open maps a
+ * handle of another process (peer access enabled on first use).
+ */
+int sp_ipc_handle(const void *ptr, void *handle64, int64_t *offset);
+int sp_ipc_open(const void *handle64, void **ptr);
+int sp_ipc_close(void *ptr);
+
+/*
+ * Stream-ordered pass counters between ranks.  sp_signal: after the stream's
+ * earlier work, fence and write `value` to `flag` (typically a neighbour's
+ * counter through peer memory).  sp_wait: later work on the stream waits until
+ * (int32)(*flag - value) >= 0.  Stream memory operations when available, else
+ * a one-thread kernel.
+ */
+int sp_signal(uint32_t *flag, uint32_t value, void *stream);
+int sp_wait(const uint32_t *flag, uint32_t value, void *stream);
+
 /* Tuning knobs (benchmarking only; results never depend on them).
  * key 0: z-chunk length for sp_sweep / sp_temporal (0 = automatic)
  * key 1: force the cp.async (non-TMA) loader when nonzero
  * key 2: tile config index per fused depth (value = levels*16 + index)
- * key 4: profiling knobs (only in builds with -DSP200_PROFILE_KNOBS=1) */
+ * key 4: profiling knobs (only in builds with -DSP200_PROFILE_KNOBS=1)
+ * key 5: sp_signal / sp_wait through kernels instead of stream memory ops */
 int sp_set_tuning(int key, int64_t value);
 
 /* Query: 1 if the TMA loader applies to a grid with row extent `ex`. */

@@ -26,7 +26,8 @@ EXPORTS = (
     "sp_version", "sp_last_error", "sp_launch_count", "sp_fill_seeded",
     "sp_fill_constant", "sp_sweep", "sp_apply_window", "sp_window_gather",
     "sp_copy_ring", "sp_rings_equal", "sp_write_faces", "sp_temporal", "sp_compressed_workspace",
-    "sp_compressed", "sp_set_tuning", "sp_tma_eligible",
+    "sp_compressed", "sp_set_tuning", "sp_tma_eligible", "sp_temporal_mirror", "sp_ipc_handle",
+    "sp_ipc_open", "sp_ipc_close", "sp_signal", "sp_wait",
 )
 
 _lib = None
@@ -58,6 +59,13 @@ def _declare(L):
         "sp_compressed": ([dp, i64, i64, i64, i64, i64, i64, i64, i32, i32, i64, i64, vp,
                            ctypes.POINTER(dp), i32, vp], i32),
         "sp_set_tuning": ([i32, i64], i32),
+        "sp_temporal_mirror": ([dp, dp, i64, i64, i64, i64, i64, i64, i64, i32, i64, i64, dp, i64, i64,
+                                vp], i32),
+        "sp_ipc_handle": ([vp, ctypes.c_char_p, ctypes.POINTER(i64)], i32),
+        "sp_ipc_open": ([ctypes.c_char_p, ctypes.POINTER(vp)], i32),
+        "sp_ipc_close": ([vp], i32),
+        "sp_signal": ([vp, ctypes.c_uint32, vp], i32),
+        "sp_wait": ([vp, ctypes.c_uint32, vp], i32),
         "sp_tma_eligible": ([i64, i64], i32),
     }
     for name, (args, res) in sig.items():

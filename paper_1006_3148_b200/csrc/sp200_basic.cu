@@ -286,6 +286,7 @@ int sp_set_tuning(int key, int64_t value) {
     case 0: t.zchunk = value; return SP_OK;
     case 1: t.force_cpasync = value; return SP_OK;
     case 4: t.debug = value; return SP_OK;
+    case 5: t.signal_kernels = value; return SP_OK;
     case 2: {
         int lv = (int)(value / 16), idx = (int)(value % 16);
         if (lv < 1 || lv > SP_MAX_FUSED) return set_error(SP_EINVAL, "bad levels in tuning");
@@ -501,6 +502,28 @@ int sp_temporal(const double *src, double *dst, int64_t ex, int64_t ey, int64_t 
     if (zlo >= zhi) return SP_OK;
     return launch_temporal(src, dst, ex, ey, ez, nx, ny, nz, off, levels, zlo, zhi, false,
                            as_stream(stream));
+}
+
+int sp_temporal_mirror(const double *src, double *dst, int64_t ex, int64_t ey, int64_t ez,
+                       int64_t nx, int64_t ny, int64_t nz, int64_t off, int levels, int64_t zlo,
+                       int64_t zhi, double *mirror, int64_t mirror_ez, int64_t mirror_zshift,
+                       void *stream) {
+    if (!src || !dst || !mirror) return set_error(SP_EINVAL, "null grid");
+    if (src == dst) return set_error(SP_EINVAL, "sp_temporal_mirror: src and dst must differ");
+    int rc = check_geom(ex, ey, ez, nx, ny, nz, off);
+    if (rc) return rc;
+    if (levels < 1 || levels > SP_MAX_FUSED)
+        return set_error(SP_EUNSUP, "levels %d outside [1, %d]", levels, SP_MAX_FUSED);
+    if (zlo < 0) zlo = 0;
+    if (zhi > nz) zhi = nz;
+    if (zlo >= zhi) return SP_OK;
+    // the mirrored storage planes must exist in the peer grid
+    if (zlo + off + mirror_zshift < 0 || zhi + off + mirror_zshift > mirror_ez)
+        return set_error(SP_EINVAL, "mirror planes [%lld, %lld) outside the peer grid (%lld planes)",
+                         (long long)(zlo + off + mirror_zshift), (long long)(zhi + off + mirror_zshift),
+                         (long long)mirror_ez);
+    return launch_temporal_mirror(src, dst, ex, ey, ez, nx, ny, nz, off, levels, zlo, zhi, mirror,
+                                  mirror_zshift, as_stream(stream));
 }
 
 int sp_tma_eligible(int64_t ex, int64_t ey) { return tma_eligible(nullptr, ex, ey) ? 1 : 0; }

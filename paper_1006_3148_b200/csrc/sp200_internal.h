@@ -19,6 +19,7 @@ struct Tuning {
     int64_t force_cpasync = 0;
     int64_t cfg_index[SP_MAX_FUSED + 1] = {0, 0, 0, 0, 0};
     int64_t debug = 0;
+    int64_t signal_kernels = 0;  // sp_signal / sp_wait through kernels, not stream memory ops
 };
 Tuning &tuning();
 
@@ -30,6 +31,10 @@ int sm_count();
 int launch_temporal(const double *src, double *dst, int64_t ex, int64_t ey, int64_t ez,
                     int64_t nx, int64_t ny, int64_t nz, int64_t off, int levels, int64_t zlo,
                     int64_t zhi, bool copy_ring, cudaStream_t stream);
+int launch_temporal_mirror(const double *src, double *dst, int64_t ex, int64_t ey, int64_t ez,
+                           int64_t nx, int64_t ny, int64_t nz, int64_t off, int levels,
+                           int64_t zlo, int64_t zhi, double *mirror, int64_t mirror_zshift,
+                           cudaStream_t stream);
 bool tma_eligible(const void *ptr, int64_t ex, int64_t ey);
 int64_t compressed_workspace(int64_t nx, int64_t ny, int64_t depth, int levels);
 int launch_compressed(double *data, int64_t ex, int64_t ey, int64_t ez, int64_t nx, int64_t ny,

@@ -56,6 +56,7 @@ struct TParams {
     int doff;        // storage offset of logical 0 in the written frame
     int direction;   // K3: +1 forward (write shifted -T), -1 backward
     double *stash_x, *stash_y, *stash_z;  // K3 band stash
+    double *mir;     // MIR: peer grid, pre-shifted so that mir + (g - dst) mirrors dst cell g
     int wx2, hy2;    // stash_x row width, stash_y rows per plane
     int debug;       // profiling only (sp_set_tuning key 4): 1 skip levels, 2 skip loads, 4 skip barrier
 };
@@ -119,7 +120,11 @@ __device__ __forceinline__ void stg2_stream(double *p, double a, double b) {
 // warps push their published row of every level 1..T-1 into the adjacent
 // CTA's halo row with st.async (DSMEM), completing a per-(level, parity)
 // mbarrier there; only the receiving boundary warp waits, one step later.
-template <int T, int CY, int R, int S, bool TMA, bool COMP, int CL>
+//
+// MIR (two-grid, unclustered): every level-T store is also issued to a peer
+// rank's grid through NVLink peer memory (z-slab halo delivery fused into the
+// pass that computes the planes, instead of a separate send/recv).
+template <int T, int CY, int R, int S, bool TMA, bool COMP, int CL, bool MIR = false>
 __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB)
     k_temporal(const TParams p, const __grid_constant__ CUtensorMap tmap) {
     using C = KCfg<T, CY, R, S>;
@@ -449,9 +454,14 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
                         double *g = dcol + (int64_t)(pout + p.doff) * pz + (int64_t)r * p.ex;
                         if (x_out[0] && x_out[1] && p.pair_store) {
                             stg2_stream(g, v[r][0], v[r][1]);
+                            if constexpr (MIR) stg2_stream(p.mir + (g - p.dst), v[r][0], v[r][1]);
                         } else {
                             if (x_out[0]) st_stream(g, v[r][0]);
                             if (x_out[1]) st_stream(g + 1, v[r][1]);
+                            if constexpr (MIR) {
+                                if (x_out[0]) st_stream(p.mir + (g - p.dst), v[r][0]);
+                                if (x_out[1]) st_stream(p.mir + (g - p.dst) + 1, v[r][1]);
+                            }
                         }
                     }
                 }
@@ -608,6 +618,8 @@ struct LaunchReq {
     int direction;  // 0: two-grid (K1/K2); +1/-1: compressed in place (K3)
     void *ws;       // K3 workspace: the band stash
     cudaStream_t stream;
+    double *mirror = nullptr;     // two-grid: peer grid receiving every stored plane
+    int64_t mirror_zshift = 0;    // storage plane z of dst -> z + zshift of mirror
 };
 
 template <int T, int CY, int CL = 1>
@@ -689,7 +701,7 @@ static void comp_layout(int64_t nx, int64_t ny, int64_t depth, int64_t off, bool
     L->nz_stash = (L->nchunks - 1) * 2 * T * ny * ((nx + 2) & ~1);
 }
 
-template <int T, int CY, int R, int S, int CL = 1>
+template <int T, int CY, int R, int S, int CL = 1, bool MIRROR = false>
 static int launch_cfg(const LaunchReq &q) {
     using C = KCfg<T, CY, R, S>;
     const bool comp = q.direction != 0;
@@ -730,7 +742,17 @@ static int launch_cfg(const LaunchReq &q) {
     p.wx2 = p.hy2 = 0;
 
     void (*kern)(const TParams, const CUtensorMap);
-    if constexpr (CL > 1) {
+    p.mir = nullptr;
+    if constexpr (MIRROR) {
+        // fused peer stores need the TMA instance; otherwise the planes are
+        // copied to the peer after the pass (same stream, DMA over NVLink)
+        if (use_tma) {
+            p.mir = q.mirror + q.mirror_zshift * q.ex * q.ey;
+            kern = k_temporal<T, CY, R, S, true, false, 1, true>;
+        } else {
+            kern = k_temporal<T, CY, R, S, false, false, 1>;
+        }
+    } else if constexpr (CL > 1) {
         kern = use_tma ? k_temporal<T, CY, R, S, true, false, CL>
                        : k_temporal<T, CY, R, S, false, false, CL>;
     } else if (comp) {
@@ -873,7 +895,46 @@ static int launch_cfg(const LaunchReq &q) {
     return rc;
 }
 
+static int dispatch(int levels, const LaunchReq &q);
+
+static bool uses_tma(const LaunchReq &q) {
+    const bool aligned =
+        ((reinterpret_cast<uintptr_t>(q.dst) | reinterpret_cast<uintptr_t>(q.src)) % 16 == 0) &&
+        (q.ex % 2 == 0);
+    return aligned && !tuning().force_cpasync && tma_eligible(q.src, q.ex, q.ey) && encode_fn();
+}
+
+// Two-grid pass whose stored planes also go to a peer rank's grid: the TMA
+// instances store them from the kernel (MIR); otherwise, and for the plain
+// sweep, the finished planes are copied after the pass on the same stream.
+static int dispatch_mirror(int levels, const LaunchReq &q) {
+    int rc;
+    const bool fused = levels > 1 && uses_tma(q);
+    switch (fused ? levels : 0) {
+    case 2: rc = launch_cfg<2, 48, 4, 4, 1, true>(q); break;
+    case 3: rc = launch_cfg<3, 36, 3, 4, 1, true>(q); break;
+    case 4: rc = launch_cfg<4, 32, 4, 4, 1, true>(q); break;
+    default: {
+        LaunchReq plain = q;
+        plain.mirror = nullptr;
+        rc = levels == 1 ? launch_sweep1(q.src, q.dst, q.ex, q.ey, q.ez, q.nx, q.ny, q.nz, q.off,
+                                         q.zlo, q.zhi, false, q.stream)
+                         : dispatch(levels, plain);
+        break;
+    }
+    }
+    if (rc || fused) return rc;
+    const int64_t pz = q.ex * q.ey;
+    const int64_t z0 = q.zlo + q.off;
+    cudaError_t e = cudaMemcpyAsync(q.mirror + (z0 + q.mirror_zshift) * pz, q.dst + z0 * pz,
+                                    (size_t)((q.zhi - q.zlo) * pz) * sizeof(double),
+                                    cudaMemcpyDeviceToDevice, q.stream);
+    if (e != cudaSuccess) return set_error(SP_ECUDA, "mirror copy: %s", cudaGetErrorString(e));
+    return SP_OK;
+}
+
 static int dispatch(int levels, const LaunchReq &q) {
+    if (q.mirror) return dispatch_mirror(levels, q);
     if (q.direction != 0) {
         // K3: the CY = 32 instances, the geometry compressed_workspace sizes
         switch (levels) {
@@ -926,6 +987,16 @@ int launch_temporal(const double *src, double *dst, int64_t ex, int64_t ey, int6
         return launch_sweep1(src, dst, ex, ey, ez, nx, ny, nz, off, zlo, zhi, copy_ring, stream);
     if (copy_ring) return set_error(SP_EUNSUP, "ring copy is fused only into the plain sweep");
     LaunchReq q{src, dst, ex, ey, ez, nx, ny, nz, off, off, zlo, zhi, 0, nullptr, stream};
+    return dispatch(levels, q);
+}
+
+int launch_temporal_mirror(const double *src, double *dst, int64_t ex, int64_t ey, int64_t ez,
+                           int64_t nx, int64_t ny, int64_t nz, int64_t off, int levels,
+                           int64_t zlo, int64_t zhi, double *mirror, int64_t mirror_zshift,
+                           cudaStream_t stream) {
+    LaunchReq q{src, dst, ex, ey, ez, nx, ny, nz, off, off, zlo, zhi, 0, nullptr, stream};
+    q.mirror = mirror;
+    q.mirror_zshift = mirror_zshift;
     return dispatch(levels, q);
 }
 

@@ -162,6 +162,21 @@ def fused_sweeps(src: Grid3, dst: Grid3, levels: int, zlo: int = 0, zhi: int | N
         int(levels), int(zlo), int(src.nz if zhi is None else zhi), _stream()), "fused_sweeps")
 
 
+def fused_sweeps_mirror(src: Grid3, dst: Grid3, levels: int, zlo: int, zhi: int, mirror_ptr: int,
+                        mirror_ez: int, mirror_zshift: int) -> None:
+    """fused_sweeps whose stored planes [zlo, zhi) also go to a peer rank's grid
+    (device pointer `mirror_ptr` with the same x/y storage extents, `mirror_ez`
+    planes) at storage plane z + zshift: the z-slab halo delivery fused into
+    the pass (sp/halo.py:239-271 for topology (1,1,P))."""
+    if src.data.shape != dst.data.shape or src.shape != dst.shape:
+        raise ValueError("grid geometry differs")
+    ex, ey, ez = src.extents
+    _lib.check(_lib.load().sp_temporal_mirror(
+        _ptr(src.data), _ptr(dst.data), ex, ey, ez, src.nx, src.ny, src.nz, src.offset,
+        int(levels), int(zlo), int(zhi), ctypes.c_void_p(int(mirror_ptr)), int(mirror_ez),
+        int(mirror_zshift), _stream()), "fused_sweeps_mirror")
+
+
 def compressed_pass(grid: Grid3, levels: int, direction: int, src_alignment: int,
                     workspace: torch.Tensor, zlo: int = 0, zhi: int | None = None,
                     side_mask: int = 63) -> None:

@@ -291,11 +291,20 @@ class PipelineEngine:
 
     # -- passes ---------------------------------------------------------------
     def _pass_two_grid(self, direction, boundary=None):
+        return _drive(self._pass_two_grid_steps(direction, boundary))
+
+    def _pass_two_grid_steps(self, direction, boundary=None):
+        """Generator form of the two-grid pass: with a fused peer boundary it
+        yields once, right before the wait that precedes the boundary stores,
+        so a driver can run every rank's first phase before any second phase
+        (run_distributed_inprocess); the return value is the launch count."""
         cfg = self.cfg
         h = cfg.h
         lives = self._lives(h)
         L0 = self.levels_done
         if not (self._fusable(lives, h) and self._check_rings_equal()):
+            if boundary is not None and getattr(boundary, "fused", False):
+                raise ValueError("peer halo delivery needs fused two-grid passes")
             # exact per-level emulation: level lvl reads grids[(lvl-1)%2] and
             # writes grids[lvl%2] over its live range (sp/pipeline.py:301-323)
             for u in range(1, h + 1):
@@ -307,10 +316,30 @@ class PipelineEngine:
         u0 = 0
         launches = 0
         chunks = split_levels(h, self.max_fused)
+        peer = boundary is not None and getattr(boundary, "fused", False)
+        if peer:
+            boundary.begin()  # neighbours' previous pass delivered our ghost planes
         for n, c in enumerate(chunks):
             zlo, zhi = lives[u0 + c][2]
             last = n == len(chunks) - 1
-            if last and boundary is not None and zhi - zlo > boundary[0] + boundary[1]:
+            if last and peer:
+                # fused peer delivery: the interior first, then the boundary
+                # planes, stored locally and into the neighbours' ghost planes
+                boundary.chunks_done()
+                blo, bhi = boundary.blo, boundary.bhi
+                if zhi - bhi > zlo + blo:
+                    fused_sweeps(cur, other, c, zlo + blo, zhi - bhi)
+                    launches += 1
+                yield
+                boundary.before_stores()
+                if blo:
+                    boundary.store(0, cur, other, c, zlo, zlo + blo)
+                    launches += 1
+                if bhi:
+                    boundary.store(1, cur, other, c, zhi - bhi, zhi)
+                    launches += 1
+                boundary.end()
+            elif last and boundary is not None and zhi - zlo > boundary[0] + boundary[1]:
                 # boundary-first: the planes the halo exchange sends are
                 # finished first, the exchange is posted, and the interior
                 # planes are computed while the transfer is in flight
@@ -390,7 +419,13 @@ class PipelineEngine:
         finish the lowest / highest z planes of the last level first and call
         post(storage, offset) before computing the rest (used by the z-slab
         driver to overlap the halo exchange with interior compute).  Without
-        the fused path, post is called after the pass."""
+        the fused path, post is called after the pass.  A FusedZHalo boundary
+        (halo.py) instead stores the boundary planes into the neighbours'
+        grids from the pass itself."""
+        return _drive(self.run_pass_steps(direction, boundary))
+
+    def run_pass_steps(self, direction: int, boundary=None):
+        """Generator form of run_pass (see _pass_two_grid_steps)."""
         cfg = self.cfg
         if direction not in (1, -1):
             raise ValueError("direction must be +1 or -1")
@@ -405,7 +440,7 @@ class PipelineEngine:
                     f"backward pass needs alignment >= h ({a0} < {cfg.h})")
             launches = self._pass_compressed(direction)
         else:
-            launches = self._pass_two_grid(direction, boundary)
+            launches = yield from self._pass_two_grid_steps(direction, boundary)
         self.levels_done += cfg.h
         self.passes_done += 1
         if cfg.grid_mode == "compressed":
@@ -414,6 +449,15 @@ class PipelineEngine:
         stats.per_thread_spins = [0] * cfg.threads
         stats.block_updates = self._total_blocks() * cfg.threads
         return stats
+
+
+def _drive(gen):
+    """Run a pass generator to completion and return its value."""
+    try:
+        while True:
+            next(gen)
+    except StopIteration as stop:
+        return stop.value
 
 
 def team_sweep(grids, cfg: PipelineConfig, direction: int = 1) -> RunStats:
