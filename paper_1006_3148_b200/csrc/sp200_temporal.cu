@@ -520,16 +520,38 @@ __device__ __forceinline__ int band_pos(int k, int o, int T2, int fwd) {
     return fwd ? (bt + 1) * o + bo : bt * o + o - T2 + bo;
 }
 
-// K3 epilogue: copy the stashed band outputs to their shifted frame, one CTA
-// per stash row (no 64-bit divisions).  The three stashes hold disjoint cell
-// sets: y band first, then z band, then x band (the order K3 stores them).
+// K3 epilogue: copy the stashed band outputs to their shifted frame.  The
+// three stashes hold disjoint cell sets: y band first, then z band, then x
+// band (the order K3 stores them).  The copies are latency-bound unless each
+// thread has several loads in flight, so every thread first loads UB values,
+// then stores them (measured: the one-value-per-iteration loops ran the x
+// stash at a quarter of the HBM rate).
+constexpr int UB = 8;
+
+__device__ __forceinline__ void copy_row_batched(double *dst, const double *src, int n) {
+    for (int b = threadIdx.x; b < n; b += UB * blockDim.x) {
+        double v[UB];
+#pragma unroll
+        for (int i = 0; i < UB; ++i) {
+            const int x = b + i * blockDim.x;
+            v[i] = x < n ? __ldcs(src + x) : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < UB; ++i) {
+            const int x = b + i * blockDim.x;
+            if (x < n) dst[x] = v[i];
+        }
+    }
+}
+
+// one CTA per stash row
 __global__ void k_unstash_y(UnstashArgs a) {
     const int k = blockIdx.x % a.hy2, zr = blockIdx.x / a.hy2;
     const int y = band_pos(k, a.oy, a.T2, a.fwd), z = a.zlo + zr;
     if (y >= a.ny) return;
     const double *src = a.sy + (int64_t)blockIdx.x * ((a.nx + 2) & ~1) + a.sxpad;
     double *dst = a.data + ((int64_t)(z + a.doff) * a.ey + (y + a.doff)) * a.ex + a.doff;
-    for (int x = threadIdx.x; x < a.nx; x += blockDim.x) dst[x] = src[x];
+    copy_row_batched(dst, src, a.nx);
 }
 
 __global__ void k_unstash_z(UnstashArgs a) {
@@ -539,44 +561,60 @@ __global__ void k_unstash_z(UnstashArgs a) {
     if (z >= a.zhi || band_hit(y - ty * a.oy, ty, a.tiles_y, a.oy, a.T2, a.fwd)) return;
     const double *src = a.sz + (int64_t)blockIdx.x * ((a.nx + 2) & ~1) + a.sxpad;
     double *dst = a.data + ((int64_t)(z + a.doff) * a.ey + (y + a.doff)) * a.ex + a.doff;
-    for (int x = threadIdx.x; x < a.nx; x += blockDim.x) dst[x] = src[x];
+    copy_row_batched(dst, src, a.nx);
 }
 
-__global__ void k_unstash_x(UnstashArgs a) {
-    // one warp per (y, z) row; lane -> (tile slot offset, column in the slot)
-    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int nrows = (a.zhi - a.zlo) * a.ny;
-    if (row >= nrows) return;
-    const int y = row % a.ny, zr = row / a.ny;
-    const int z = a.zlo + zr;
-    const int ty = y / a.oy;
-    if (band_hit(y - ty * a.oy, ty, a.tiles_y, a.oy, a.T2, a.fwd)) return;
-    const int zo = zr % a.zc, chunk = zr / a.zc;
-    const int zlen = min(a.zc, a.zhi - a.zlo - chunk * a.zc);
-    if (a.fwd ? (chunk > 0 && zo < a.T2) : (chunk < a.nchunks - 1 && zo >= zlen - a.T2)) return;
-    const double *src = a.sx + (int64_t)row * a.wx2;
-    double *dst = a.data + ((int64_t)(z + a.doff) * a.ey + (y + a.doff)) * a.ex + a.doff;
+// x stash: CTA = UX_ROWS rows y of one plane z (blockIdx.y); thread x =
+// stash column (tile slot bt, column kk of the slot), thread y + 2i = row i of
+// the UB rows it copies.  Rows inside the y or z band belong to the other
+// stashes and are skipped.  No per-row divisions: the index math is a large
+// share of this kernel's instructions otherwise.
+constexpr int UX_ROWS = 2 * UB;
+__global__ void __launch_bounds__(256) k_unstash_x(UnstashArgs a) {
+    const int zr = blockIdx.y, z = a.zlo + zr;
+    {
+        const int zo = zr % a.zc, chunk = zr / a.zc;
+        const int zlen = min(a.zc, a.zhi - a.zlo - chunk * a.zc);
+        if (a.fwd ? (chunk > 0 && zo < a.T2) : (chunk < a.nchunks - 1 && zo >= zlen - a.T2)) return;
+    }
+    const int y0 = blockIdx.x * UX_ROWS + threadIdx.y;
+    int ty = y0 / a.oy, yo = y0 - ty * a.oy;
+    const int64_t srow0 = ((int64_t)zr * a.ny + y0) * a.wx2;
+    const int64_t drow0 = ((int64_t)(z + a.doff) * a.ey + (y0 + a.doff)) * a.ex + a.doff;
+    unsigned live = 0;
+#pragma unroll
+    for (int i = 0; i < UB; ++i) {
+        if (y0 + 2 * i < a.ny && !band_hit(yo, ty, a.tiles_y, a.oy, a.T2, a.fwd)) live |= 1u << i;
+        yo += 2;
+        while (yo >= a.oy) {
+            yo -= a.oy;
+            ++ty;
+        }
+    }
     // stash column kk of tile slot bt holds stored-tile column lo + kk,
     // lo = -e (forward) or ox - 2T - e (backward); the forward band ends with
     // the lane pair that starts below 2T (see the x band in k_temporal)
     const int xbw = a.T2 + 2, e = a.sxpad;
-    const int per = 32 / xbw, lane = threadIdx.x & 31;
-    const int boff = lane / xbw, kk = lane - boff * xbw;
-    if (boff >= per) return;
-    int xo;
-    bool ok;
-    if (a.fwd) {
-        ok = (kk & ~1) - e < a.T2;
-        xo = kk - e;
-    } else {
-        ok = true;
-        xo = a.ox - a.T2 - e + kk;
-    }
-    ok = ok && xo >= 0 && xo < a.ox;
-    const int nslots = a.wx2 / xbw;
-    for (int bt = boff; bt < nslots; bt += per) {
+    for (int c = threadIdx.x; c < a.wx2; c += blockDim.x) {
+        const int bt = c / xbw, kk = c - bt * xbw;
+        int xo;
+        bool ok;
+        if (a.fwd) {
+            ok = (kk & ~1) - e < a.T2;
+            xo = kk - e;
+        } else {
+            ok = true;
+            xo = a.ox - a.T2 - e + kk;
+        }
         const int x = (a.fwd ? bt + 1 : bt) * a.ox + xo;
-        if (ok && x < a.nx) dst[x] = src[bt * xbw + kk];
+        ok = ok && xo >= 0 && xo < a.ox && x < a.nx;
+        double v[UB];
+#pragma unroll
+        for (int i = 0; i < UB; ++i)
+            v[i] = (ok && ((live >> i) & 1u)) ? __ldcs(a.sx + srow0 + (int64_t)(2 * i) * a.wx2 + c) : 0.0;
+#pragma unroll
+        for (int i = 0; i < UB; ++i)
+            if (ok && ((live >> i) & 1u)) a.data[drow0 + (int64_t)(2 * i) * a.ex + x] = v[i];
     }
 }
 
@@ -888,7 +926,8 @@ static int launch_cfg(const LaunchReq &q) {
         count_launch();
     }
     if (L.wx2 > 0) {
-        k_unstash_x<<<(unsigned)((depth_ * q.ny + 7) / 8), 256, 0, q.stream>>>(u);
+        k_unstash_x<<<dim3((unsigned)((q.ny + UX_ROWS - 1) / UX_ROWS), (unsigned)depth_), dim3(128, 2), 0,
+                      q.stream>>>(u);
         count_launch();
     }
     rc = check_launch("k_unstash");
