@@ -115,17 +115,17 @@ class Clocks:
 # reference arm / cpu baseline: the oracle's C port of reference_sweep
 # ---------------------------------------------------------------------------
 
-def cpu_rate(target_s: float = 12.0, max_sweeps: int = 100):
-    """Time the reference CPU path (oracle C port of sp/kernel.py:99-111, all
-    host threads) on the C2 grid for ~target_s seconds.  Returns
-    (GLUP/s, threads, sample description)."""
-    import numpy as np  # noqa: F401
+def _cpu_child(target_s: float, max_sweeps: int = 100) -> int:
+    """Child of cpu_rate: time the reference CPU path (oracle C port of
+    sp/kernel.py:99-111, all host threads) on the C2 grid for ~target_s
+    seconds in a process without torch or a CUDA context; print one JSON."""
     import oracle
     n = (N_INT, N_INT, N_INT)
     d = oracle.make_storage(*n, init="random", seed=SEED)
     a, b = d, d.copy()
-    L = oracle.lib()
-    threads = L.or_max_threads()
+    threads = oracle.lib().or_max_threads()
+    oracle.c_sweeps(a, b, n, 1, threads=threads)  # first touch, thread pool
+    a, b = b, a
     done = 0
     t0 = time.perf_counter()
     while done < max_sweeps:
@@ -135,10 +135,21 @@ def cpu_rate(target_s: float = 12.0, max_sweeps: int = 100):
         if time.perf_counter() - t0 >= target_s:
             break
     dt = time.perf_counter() - t0
-    rate = N_INT ** 3 * done / dt / 1e9
-    sample = (f"{done} reference sweeps of the 512^3 C2 grid (oracle C port of reference_sweep, "
-              f"OpenMP over z, {threads} threads) in {dt:.1f} s")
-    return rate, threads, sample
+    print(json.dumps({"rate": N_INT ** 3 * done / dt / 1e9, "threads": threads, "done": done, "dt": dt}))
+    return 0
+
+
+def cpu_rate(target_s: float = 12.0, max_sweeps: int = 100):
+    """Time the reference CPU path in a separate process (the bench process
+    holds torch's thread pool, a CUDA context and the clock sampler; run in
+    it the OpenMP sweep measured about half of the reference arm's rate).
+    Returns (GLUP/s, threads, sample description)."""
+    out = subprocess.run([sys.executable, os.path.abspath(__file__), "--cpu-child", str(target_s)],
+                         capture_output=True, text=True, check=True).stdout
+    r = json.loads(out.strip().splitlines()[-1])
+    sample = (f"{r['done']} reference sweeps of the 512^3 C2 grid (oracle C port of reference_sweep, "
+              f"OpenMP over z, {r['threads']} threads) in {r['dt']:.1f} s, separate process")
+    return r["rate"], r["threads"], sample
 
 
 def run_reference_arm(args):
@@ -535,12 +546,15 @@ def main():
     ap.add_argument("--quick", action="store_true", help="skip per-depth and e2e legs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-child", type=float, default=None, help=argparse.SUPPRESS)
     ap.add_argument("--ref-sweeps-per-step", type=int, default=2)
     ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
                     help="z-slab halo delivery for N>1: NCCL P2P, or the fused peer-memory stores")
     ap.add_argument("--slab", action="store_true",
                     help="use the distributed z-slab driver even on one GPU (path check)")
     args = ap.parse_args()
+    if args.cpu_child is not None:
+        return _cpu_child(args.cpu_child)
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":
         return run_reference_arm(args)
