@@ -227,36 +227,44 @@ struct FaceArgs {
 };
 
 // faces: (x,0),(x,1): [nz][ny]; (y,0),(y,1): [nz][nx]; (z,0),(z,1): [ny][nx]
+// One face row per CTA row (blockIdx.y strides over the 2nz + 2nz + 2ny face
+// rows; comparisons pick the face), threads along the row: no per-element
+// 64-bit division.  The earlier flat-index form spent most of its 42 us per
+// call (600^3) in the div/mod chain.
 __global__ void k_write_faces(FaceArgs a) {
-    const int64_t nxf = a.nz * a.ny, nyf = a.nz * a.nx, nzf = a.ny * a.nx;
-    const int64_t total = 2 * (nxf + nyf + nzf);
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t nrows = 4 * a.nz + 2 * a.ny;
+    for (int64_t row = blockIdx.y; row < nrows; row += gridDim.y) {
         int face;
-        int64_t r, x, y, z;
-        if (idx < 2 * nxf) {
-            face = (int)(idx / nxf);
-            r = idx % nxf;
-            z = a.off + r / a.ny;
-            y = a.off + r % a.ny;
-            x = face ? a.off + a.nx : a.off - 1;
-        } else if (idx < 2 * (nxf + nyf)) {
-            int64_t q = idx - 2 * nxf;
-            face = 2 + (int)(q / nyf);
-            r = q % nyf;
-            z = a.off + r / a.nx;
-            x = a.off + r % a.nx;
-            y = (face & 1) ? a.off + a.ny : a.off - 1;
+        int64_t r0, len, base, step;  // face-array row start, length, storage base/stride
+        if (row < 2 * a.nz) {
+            face = row >= a.nz;
+            const int64_t z = row - face * a.nz;
+            r0 = z * a.ny;
+            len = a.ny;
+            base = ((a.off + z) * a.ey + a.off) * a.ex + (face ? a.off + a.nx : a.off - 1);
+            step = a.ex;
+        } else if (row < 4 * a.nz) {
+            const int64_t q = row - 2 * a.nz;
+            face = 2 + (q >= a.nz);
+            const int64_t z = q - (face - 2) * a.nz;
+            r0 = z * a.nx;
+            len = a.nx;
+            base = ((a.off + z) * a.ey + ((face & 1) ? a.off + a.ny : a.off - 1)) * a.ex + a.off;
+            step = 1;
         } else {
-            int64_t q = idx - 2 * (nxf + nyf);
-            face = 4 + (int)(q / nzf);
-            r = q % nzf;
-            y = a.off + r / a.nx;
-            x = a.off + r % a.nx;
-            z = (face & 1) ? a.off + a.nz : a.off - 1;
+            const int64_t q = row - 4 * a.nz;
+            face = 4 + (q >= a.ny);
+            const int64_t y = q - (face - 4) * a.ny;
+            r0 = y * a.nx;
+            len = a.nx;
+            base = (((face & 1) ? a.off + a.nz : a.off - 1) * a.ey + a.off + y) * a.ex + a.off;
+            step = 1;
         }
         if (!((a.mask >> face) & 1)) continue;
-        a.d[(z * a.ey + y) * a.ex + x] = a.f[face][r];
+        const double *f = a.f[face] + r0;
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
+             i += (int64_t)gridDim.x * blockDim.x)
+            a.d[base + i * step] = f[i];
     }
 }
 
@@ -472,8 +480,9 @@ int sp_write_faces(double *data, int64_t ex, int64_t ey, int64_t ez, int64_t nx,
         if (((a.mask >> f) & 1) && !faces[f]) return set_error(SP_EINVAL, "null face %d", f);
     }
     if (!a.mask) return SP_OK;
-    int64_t total = 2 * (nz * ny + nz * nx + ny * nx);
-    k_write_faces<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(a);
+    const int64_t len = nx > ny ? nx : ny, nrows = 4 * nz + 2 * ny;
+    dim3 grid((unsigned)((len + 127) / 128), (unsigned)(nrows < 65535 ? nrows : 65535));
+    k_write_faces<<<grid, 128, 0, as_stream(stream)>>>(a);
     count_launch();
     return check_launch("sp_write_faces");
 }

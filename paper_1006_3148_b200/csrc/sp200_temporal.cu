@@ -124,10 +124,17 @@ __device__ __forceinline__ void stg2_stream(double *p, double a, double b) {
 // MIR (two-grid, unclustered): every level-T store is also issued to a peer
 // rank's grid through NVLink peer memory (z-slab halo delivery fused into the
 // pass that computes the planes, instead of a separate send/recv).
-template <int T, int CY, int R, int S, bool TMA, bool COMP, int CL, bool MIR = false>
+//
+// WP (TMA only): level 1 reads its own level-0 values of the current and the
+// previous plane from the stage ring instead of keeping them in registers
+// (W0, 4R doubles per thread).  The prefetch distance drops to S-2 so the
+// previous plane's stage is not refilled while it is still read.
+template <int T, int CY, int R, int S, bool TMA, bool COMP, int CL, bool MIR = false, bool WP = false>
 __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB)
     k_temporal(const TParams p, const __grid_constant__ CUtensorMap tmap) {
     using C = KCfg<T, CY, R, S>;
+    static_assert(!WP || (TMA && S >= 4), "WP: TMA loader, at least 4 stages");
+    constexpr int PD = WP ? S - 2 : S - 1;  // stage prefetch distance
     constexpr int SPX = C::SPX, C0 = C::C0, PLANE = C::PLANE, PLANE_AL = C::PLANE_AL,
                   NT = C::NT;
     constexpr int NW = NT / 32;
@@ -300,7 +307,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
 
     if constexpr (TMA) {
         if (tid == 0 && !(SP200_PROFILE_KNOBS && (p.debug & 2)))
-            for (int s = 0; s < S - 1; ++s)
+            for (int s = 0; s < PD; ++s)
                 if (s < nload) issue(s);
     } else {
         for (int s = 0; s < S - 1; ++s) {
@@ -315,7 +322,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     // loop is unrolled by two) so the register rotation is pure renaming.
     // MODE 0: every cell interior (no select); 1: static x/y Dirichlet mask;
     // 2: mask plus per-level z-ring planes (domain z ends only).
-    auto levels = [&](int s, const double *cur, auto Qc, auto Mc) {
+    auto levels = [&](int s, const double *cur, const double *prv, auto Qc, auto Mc) {
         constexpr int Q = decltype(Qc)::value;
         constexpr int MODE = decltype(Mc)::value;
 #pragma unroll
@@ -362,10 +369,18 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
             // five dependent adds stage by stage across all cells so that the
             // 8-cycle DADD latency is covered by independent work of this warp
             double A[R][2], xl[R], xr[R];
+            [[maybe_unused]] double wp[R][2];
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 A[r][0] = (u == 1) ? st.W0[Q][r][0] : st.P[ui][Q ^ 1][r][0];
                 A[r][1] = (u == 1) ? st.W0[Q][r][1] : st.P[ui][Q ^ 1][r][1];
+                if constexpr (WP) {
+                    if (u == 1) {
+                        const double2 a = lds2(prv + (j0 + r + 1) * SPX + C0 + i0);
+                        wp[r][0] = a.x;
+                        wp[r][1] = a.y;
+                    }
+                }
             }
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -403,7 +418,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
             for (int r = 0; r < R; ++r)
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
-                    const double wl = (u == 1) ? st.W0[Q ^ 1][r][c] : st.P[ui][Q][r][c];
+                    const double wl = (u == 1) ? (WP ? wp[r][c] : st.W0[Q ^ 1][r][c]) : st.P[ui][Q][r][c];
                     v[r][c] = dmul(v[r][c], 1.0 / 6.0);
                     // level T values are stored only for interior cells
                     if constexpr (MODE == 1) {
@@ -478,19 +493,22 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
         }
         if (!(SP200_PROFILE_KNOBS && (p.debug & 4))) __syncthreads();
         if constexpr (TMA) {
-            if (tid == 0 && s + S - 1 < nload && !(SP200_PROFILE_KNOBS && (p.debug & 2))) issue(s + S - 1);
+            if (tid == 0 && s + PD < nload && !(SP200_PROFILE_KNOBS && (p.debug & 2))) issue(s + PD);
         } else {
             if (s + S - 1 < nload) issue(s + S - 1);
             else cp_async_commit();
         }
         const double *cur = stage + si * PLANE_AL;
+        // WP: the previous plane's stage (the current one at s = 0: that
+        // step's level-1 output plane is below the valid range anyway)
+        const double *prv = (WP && s > 0) ? stage + (int)((gbase + s + S - 1) % S) * PLANE_AL : cur;
         // every level's finished plane inside [0, nz): no z-ring this step
         const int pmax = z0 - T + s - 1, pmin = z0 - T + s - 2 * T + 1;
         const bool zall = (pmin >= 0) && (pmax < p.nz);
         if (SP200_PROFILE_KNOBS && (p.debug & 1)) return;  // profiling builds only
-        if (wint && zall) levels(s, cur, Qc, IC<0>{});
-        else if (zall) levels(s, cur, Qc, IC<1>{});
-        else levels(s, cur, Qc, IC<2>{});
+        if (wint && zall) levels(s, cur, prv, Qc, IC<0>{});
+        else if (zall) levels(s, cur, prv, Qc, IC<1>{});
+        else levels(s, cur, prv, Qc, IC<2>{});
     };
 
     for (int s = 0; s < nsteps; s += 2) {
@@ -739,7 +757,7 @@ static void comp_layout(int64_t nx, int64_t ny, int64_t depth, int64_t off, bool
     L->nz_stash = (L->nchunks - 1) * 2 * T * ny * ((nx + 2) & ~1);
 }
 
-template <int T, int CY, int R, int S, int CL = 1, bool MIRROR = false>
+template <int T, int CY, int R, int S, int CL = 1, bool MIRROR = false, bool WP = false>
 static int launch_cfg(const LaunchReq &q) {
     using C = KCfg<T, CY, R, S>;
     const bool comp = q.direction != 0;
@@ -796,7 +814,7 @@ static int launch_cfg(const LaunchReq &q) {
     } else if (comp) {
         kern = use_tma ? k_temporal<T, CY, R, S, true, true, 1> : k_temporal<T, CY, R, S, false, true, 1>;
     } else {
-        kern = use_tma ? k_temporal<T, CY, R, S, true, false, 1>
+        kern = use_tma ? k_temporal<T, CY, R, S, true, false, 1, false, WP>
                        : k_temporal<T, CY, R, S, false, false, 1>;
     }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1012,6 +1030,7 @@ static int dispatch(int levels, const LaunchReq &q) {
         case 3: return launch_cfg<4, 24, 2, 4>(q);
         case 4: return launch_cfg<4, 32, 4, 4, 2>(q);
         case 5: return launch_cfg<4, 36, 3, 4>(q);
+        case 6: return launch_cfg<4, 32, 4, 5, 1, false, true>(q);  // WP: 735 vs 770 GLUP/s
         default: return launch_cfg<4, 32, 4, 4>(q);  // 8 warps x 254 registers
         }
     default:

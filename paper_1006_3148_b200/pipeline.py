@@ -225,6 +225,10 @@ class PipelineEngine:
         self.physical_sides = physical_sides
         self.levels_done = 0
         self.passes_done = 0
+        # (storage pointer, alignment) of the face ring the last fused
+        # compressed pass wrote; trusted only while run_pipelined drives
+        self._faces_frame = None
+        self._faces_trusted = False
         self._rings_equal = None
         self._plans = None
 
@@ -378,8 +382,13 @@ class PipelineEngine:
         for n, (axis, side) in enumerate((("x", 0), ("x", 1), ("y", 0), ("y", 1), ("z", 0), ("z", 1))):
             if self.physical_sides["xyz".index(axis)][side]:
                 mask |= 1 << n
-        # _write_full_ring (sp/pipeline.py:427-447) at the pass's source frame
-        write_faces(g, g.origin - a0, mask)
+        # _write_full_ring (sp/pipeline.py:427-447) at the pass's source frame.
+        # Inside run_pipelined the previous fused pass already left the faces
+        # at exactly this frame (no caller code runs in between), so the
+        # rewrite would store the same values again.
+        if not (self._faces_trusted and self._faces_frame == (g.data.data_ptr(), a0)):
+            write_faces(g, g.origin - a0, mask)
+        self._faces_frame = None
         lives = self._lives(h)
         if self._fusable(lives, h):
             # K3: fused in-place passes; each leaves the faces at its new frame
@@ -392,6 +401,7 @@ class PipelineEngine:
                 launches += 2
                 a += s * c
                 u0 += c
+            self._faces_frame = (g.data.data_ptr(), a)
             return launches
         sides = [(name, side) for ax, name in enumerate("xyz") for side in (0, 1)
                  if self.physical_sides[ax][side]]
@@ -472,6 +482,7 @@ def run_pipelined(grids, cfg: PipelineConfig, total_passes: int) -> RunStats:
     work on other streams (e.g. host transfers of the next input) keeps
     running."""
     engine = PipelineEngine(cfg, grids)
+    engine._faces_trusted = True
     if cfg.grid_mode == "compressed":
         if total_passes % 2 != 0:
             raise ValueError("compressed mode needs an even number of passes")
