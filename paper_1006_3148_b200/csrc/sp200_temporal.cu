@@ -285,6 +285,12 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     double *sy_col = COMP ? p.stash_y + ((int64_t)ky0 - (int64_t)p.zlo * p.hy2) * srow + rx0 + i0 + sxpad
                           : nullptr;
     double *sz_col = COMP ? p.stash_z + (int64_t)(ry0 + j0) * srow + rx0 + i0 + sxpad : nullptr;
+    // per-step band tests and stash rows reduce to one compare and one
+    // multiply-add each: z band = output planes zo in [zb_lo, zb_lo + 2T) of
+    // the chunk, z stash plane kz = zo + kz_off
+    const int zb_lo = fwd ? 0 : (z1 - z0) - 2 * T;
+    const int kz_off = fwd ? (chunk - 1) * 2 * T : chunk * 2 * T - ((z1 - z0) - 2 * T);
+    const int64_t ystride = (int64_t)p.hy2 * srow, zstride = (int64_t)p.ny * srow;
 
     auto issue = [&](int s) {
         const int si = (int)((gbase + s) % S);
@@ -359,10 +365,9 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
                 if (u == T) {
                     nrow = ncol + (int64_t)pout * npz;
                     const int zo = pout - z0;
-                    zb = zband_chunk && (fwd ? zo < 2 * T : zo >= (z1 - z0) - 2 * T);
-                    const int kz = fwd ? (chunk - 1) * 2 * T + zo : chunk * 2 * T + zo - ((z1 - z0) - 2 * T);
-                    yrow = sy_col + (int64_t)pout * p.hy2 * srow;
-                    zrow = sz_col + (int64_t)kz * p.ny * srow;
+                    zb = zband_chunk && (unsigned)(zo - zb_lo) < (unsigned)(2 * T);
+                    zrow = sz_col + (int64_t)(zo + kz_off) * zstride;
+                    yrow = sy_col + (int64_t)pout * ystride;
                 }
             }
             // gather the level u-1 inputs of all 2R cells first, then run the
