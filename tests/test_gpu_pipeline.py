@@ -227,6 +227,25 @@ def test_compressed_fused_in_place(dims, t, passes):
     assert g.alignment == 0
 
 
+def test_compressed_faces_rewritten_after_caller_edits():
+    """Inside one run_pipelined the fused passes skip the source-frame face
+    rewrite (the previous pass left the faces there); a new call must write
+    them again (_write_full_ring, sp/pipeline.py:427-447): poison everything
+    outside the interior between calls and the result must not change."""
+    dims, t = (70, 40, 30), 4
+    d0 = oracle.make_storage(*dims, init="random", seed=5, ring=0.25)
+    g = sp.create_grid(*dims, pad=t, init="random", seed=5, ring=0.25)
+    cfg = sp.PipelineConfig(spec=sp.BlockSpec(dims[0], 4, 4), t=t, grid_mode="compressed")
+    sp.run_pipelined(g, cfg, 4)
+    assert_bitwise(g.interior_numpy(), oracle.interior(oracle.sweeps(d0, dims, 4 * t), *dims))
+    keep = g.interior_view().clone()
+    g.data.fill_(float("nan"))
+    g.interior_view().copy_(keep)
+    sp.run_pipelined(g, cfg, 2)
+    assert_bitwise(g.interior_numpy(), oracle.interior(oracle.sweeps(d0, dims, 6 * t), *dims))
+    assert g.alignment == 0
+
+
 @pytest.mark.slow
 def test_large_config_c4_single_gpu(golden):
     """BASELINE configs[3] at P=1: 1024^3, ring 1.0, 40 sweeps (t=4 x10) —
