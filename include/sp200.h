@@ -196,7 +196,9 @@ int sp_wait(const uint32_t *flag, uint32_t value, void *stream);
  * key 1: force the cp.async (non-TMA) loader when nonzero
  * key 2: tile config index per fused depth (value = levels*16 + index)
  * key 4: profiling knobs (only in builds with -DSP200_PROFILE_KNOBS=1)
- * key 5: sp_signal / sp_wait through kernels instead of stream memory ops */
+ * key 5: sp_signal / sp_wait through kernels instead of stream memory ops
+ * key 6: split K2 passes as two launches (full columns, then z-chunks)
+ *        instead of one grid (A/B only) */
 int sp_set_tuning(int key, int64_t value);
 
 /* Query: 1 if the TMA loader applies to a grid with row extent `ex`. */

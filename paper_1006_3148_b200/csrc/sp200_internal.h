@@ -20,6 +20,7 @@ struct Tuning {
     int64_t cfg_index[SP_MAX_FUSED + 1] = {0, 0, 0, 0, 0};
     int64_t debug = 0;
     int64_t signal_kernels = 0;  // sp_signal / sp_wait through kernels, not stream memory ops
+    int64_t two_launch = 0;      // K2 split pass as two launches instead of one split grid
 };
 Tuning &tuning();
 

@@ -52,6 +52,9 @@ struct TParams {
     int pair_store;  // 16-byte aligned column pairs in global memory
     int tiles_x, tiles_y, ntiles;
     int tile_base, tile_count;  // tiles [tile_base, tile_base+tile_count) in this launch
+    // two-grid split launch: CTAs from `split` on cover tiles
+    // [tile_base2, tile_base2+tile_count2) in z-chunks of zc2 planes
+    int split, tile_base2, tile_count2, zc2;
     int zlo, zhi, zc;
     int doff;        // storage offset of logical 0 in the written frame
     int direction;   // K3: +1 forward (write shifted -T), -1 backward
@@ -204,10 +207,13 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     // running CTAs cover neighbouring tiles at the same z range and the
     // overlapped halo reads hit L2
     const int cid = (int)(blockIdx.x / CL);
-    const int tile = p.tile_base + cid % p.tile_count;
-    const int chunk = cid / p.tile_count;
-    const int z0 = p.zlo + chunk * p.zc;
-    const int z1 = min(z0 + p.zc, p.zhi);
+    const bool second = !COMP && cid >= p.split;
+    const int ucid = second ? cid - p.split : cid;
+    const int tcount = second ? p.tile_count2 : p.tile_count, uzc = second ? p.zc2 : p.zc;
+    const int tile = (second ? p.tile_base2 : p.tile_base) + ucid % tcount;
+    const int chunk = ucid / tcount;
+    const int z0 = p.zlo + chunk * uzc;
+    const int z1 = min(z0 + uzc, p.zhi);
     const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
     const int x0 = tx * p.ox, y0 = ty * OYc;
     // logical coords of this CTA's region (0, 0)
@@ -889,6 +895,8 @@ static int launch_cfg(const LaunchReq &q) {
     }
     p.tile_base = 0;
     p.tile_count = p.ntiles;
+    p.split = 0x7fffffff;
+    p.tile_base2 = p.tile_count2 = p.zc2 = 0;
     if (grid * CL > 0x7fffffff) return set_error(SP_EUNSUP, "grid too large");
 
     CUtensorMap tmap;
@@ -911,6 +919,24 @@ static int launch_cfg(const LaunchReq &q) {
         // tiles at the same z at the same time (L2 catches the halos).
         const int full = (int)((p.ntiles / slots) * slots);
         const int rem = p.ntiles - full;
+        if (!tuning().two_launch && rem > 0) {
+            // one grid: the chunk CTAs follow the full-column CTAs in
+            // blockIdx order, so each starts on the first SM that frees up
+            // instead of behind the slowest full column (no kernel boundary)
+            TParams a = p;
+            a.tile_base = 0;
+            a.tile_count = full;
+            a.zc = (int)depth;
+            a.split = full;
+            a.tile_base2 = full;
+            a.tile_count2 = rem;
+            const int64_t zcb = pick_zchunk(depth, rem, slots, T);
+            a.zc2 = (int)zcb;
+            const int64_t gb = (int64_t)rem * ((depth + zcb - 1) / zcb);
+            launch_units<CL>(kern, full + gb, C::NT, C::SMEM, q.stream, a, tmap);
+            count_launch();
+            return check_launch("k_temporal");
+        }
         TParams a = p;
         a.tile_base = 0;
         a.tile_count = full;

@@ -22,9 +22,13 @@ ap.add_argument("--n", type=int, default=512)
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--no-check", action="store_true")
 ap.add_argument("--debug", type=int, default=0, help="sp_set_tuning key 4 (profiling builds)")
+ap.add_argument("--tune", default="", help="extra sp_set_tuning pairs, e.g. 6=1")
 a = ap.parse_args()
 L = sp._lib.load()
 L.sp_set_tuning(4, a.debug)
+for kv in filter(None, a.tune.split(",")):
+    k, v = kv.split("=")
+    L.sp_set_tuning(int(k), int(v))
 cfgs = [int(c) for c in a.cfgs.split(",")]
 ts = [int(t) for t in a.ts.split(",")]
 
