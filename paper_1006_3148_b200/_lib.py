@@ -84,6 +84,11 @@ def load(path: str = LIB_PATH):
                 "`python -m paper_1006_3148_b200._build` (there is no CPU fallback)")
         L = ctypes.CDLL(path)
         _declare(L)
+        # A/B experiments only: SP200_TUNE="key=value,..." (sp_set_tuning)
+        for kv in filter(None, os.environ.get("SP200_TUNE", "").split(",")):
+            k, v = kv.split("=")
+            if L.sp_set_tuning(int(k), int(v)) != SP_OK:
+                raise ValueError(f"SP200_TUNE: bad pair {kv!r}")
         _lib = L
     return _lib
 
