@@ -348,7 +348,7 @@ int launch_sweep1(const double *src, double *dst, int64_t ex, int64_t ey, int64_
     case 1: return k1::launch_cfg<1, 2, 32, 4, 4>(src, dst, ex, ey, ez, nx, ny, nz, off, zlo, zhi, copy_ring, stream);
     case 2: return k1::launch_cfg<1, 1, 16, 2, 8>(src, dst, ex, ey, ez, nx, ny, nz, off, zlo, zhi, copy_ring, stream);
     case 3: return k1::launch_cfg<1, 2, 16, 1, 6>(src, dst, ex, ey, ez, nx, ny, nz, off, zlo, zhi, copy_ring, stream);
-    default: return k1::launch_cfg<1, 2, 16, 2, 6>(src, dst, ex, ey, ez, nx, ny, nz, off, zlo, zhi, copy_ring, stream);
+    default: return k1::launch_cfg<1, 2, 16, 2, 6>(src, dst, ex, ey, ez, nx, ny, nz, off, zlo, zhi, copy_ring, stream);  // 4: A/B
     }
 }
 

@@ -888,7 +888,20 @@ static int launch_cfg(const LaunchReq &q) {
     } else {
         // z-chunking: choose the chunk count minimising (waves x steps per chunk)
         int64_t zc = tuning().zchunk;
-        if (zc <= 0) zc = pick_zchunk(depth, p.ntiles, slots, T);
+        // T = 1 (plain sweep, HBM-bound): short chunks of about 12 planes
+        // keep concurrently running CTAs at the same z, so their streams
+        // share DRAM pages; with 15+ waves of 2 CTAs per SM the wave
+        // quantisation of the model below does not matter (512^3: 8 / 12 /
+        // 16 / 32 / 64 planes 387 / 393 / 385 / 373 / 345 GLUP/s; whole
+        // columns 274)
+        if (zc <= 0) {
+            if (T == 1) {
+                const int64_t c = (depth + 11) / 12;
+                zc = (depth + c - 1) / c;
+            } else {
+                zc = pick_zchunk(depth, p.ntiles, slots, T);
+            }
+        }
         if (zc < 1) zc = 1;
         p.zc = (int)zc;
         grid = (int64_t)p.ntiles * ((depth + zc - 1) / zc);
@@ -912,7 +925,7 @@ static int launch_cfg(const LaunchReq &q) {
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return set_error(SP_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     }
-    if (!comp && tuning().zchunk <= 0 && p.ntiles >= slots) {
+    if (!comp && T > 1 && tuning().zchunk <= 0 && p.ntiles >= slots) {
         // Two launches: whole slots-worth of tiles march their full column
         // (no pipeline restarts), the remaining tiles are split into z-chunks
         // so that together they fill one more wave.  Both keep neighbouring
@@ -1022,9 +1035,10 @@ static int dispatch_mirror(int levels, const LaunchReq &q) {
     default: {
         LaunchReq plain = q;
         plain.mirror = nullptr;
-        rc = levels == 1 ? launch_sweep1(q.src, q.dst, q.ex, q.ey, q.ez, q.nx, q.ny, q.nz, q.off,
-                                         q.zlo, q.zhi, false, q.stream)
-                         : dispatch(levels, plain);
+        rc = (levels == 1 && tuning().cfg_index[1] != 0)
+                 ? launch_sweep1(q.src, q.dst, q.ex, q.ey, q.ez, q.nx, q.ny, q.nz, q.off, q.zlo, q.zhi,
+                                 false, q.stream)
+                 : dispatch(levels, plain);
         break;
     }
     }
@@ -1089,10 +1103,14 @@ static int dispatch(int levels, const LaunchReq &q) {
 int launch_temporal(const double *src, double *dst, int64_t ex, int64_t ey, int64_t ez,
                     int64_t nx, int64_t ny, int64_t nz, int64_t off, int levels, int64_t zlo,
                     int64_t zhi, bool copy_ring, cudaStream_t stream) {
-    if (levels == 1)
+    LaunchReq q{src, dst, ex, ey, ez, nx, ny, nz, off, off, zlo, zhi, 0, nullptr, stream};
+    // plain sweeps: the depth-1 instance of this kernel (lane pairs, 2 CTAs
+    // per SM, 8-16-plane z-chunks) unless the ring copy of reference_sweep is
+    // fused in, which k_sweep1 does; tuning key 2 (levels 1, index 1-4)
+    // selects the k_sweep1 variants for A/B
+    if (levels == 1 && (copy_ring || tuning().cfg_index[1] != 0))
         return launch_sweep1(src, dst, ex, ey, ez, nx, ny, nz, off, zlo, zhi, copy_ring, stream);
     if (copy_ring) return set_error(SP_EUNSUP, "ring copy is fused only into the plain sweep");
-    LaunchReq q{src, dst, ex, ey, ez, nx, ny, nz, off, off, zlo, zhi, 0, nullptr, stream};
     return dispatch(levels, q);
 }
 

@@ -20,12 +20,14 @@ SHAPES = [(90, 61, 30), (130, 130, 20), (37, 100, 17), (64, 5, 9), (70, 200, 12)
 def lib():
     L = sp._lib.load()
     yield L
-    for t in range(2, 5):
+    for t in range(1, 5):
         L.sp_set_tuning(2, t * 16)
+    L.sp_set_tuning(6, 0)
 
 
-@pytest.mark.parametrize("levels", [2, 3, 4])
-@pytest.mark.parametrize("idx", [0, 1, 2, 3, 4, 5])
+@pytest.mark.parametrize("levels,idx", [(lv, i) for lv in (2, 3, 4) for i in range(6)] +
+                         [(4, 6)] +                                   # WP: level 0 from the stage ring
+                         [(1, i) for i in range(5)])                  # 0: k_temporal<1>, 1-4: k_sweep1
 def test_kernel_variants(lib, levels, idx):
     assert lib.sp_set_tuning(2, levels * 16 + idx) == 0
     for dims in SHAPES:
@@ -42,3 +44,17 @@ def test_kernel_variants(lib, levels, idx):
         got = dst2.interior_numpy()
         assert_bitwise(got[zlo:zhi], exp[zlo:zhi])
         assert np.all(got[:zlo] == -3.0) and np.all(got[zhi:] == -3.0)
+
+
+@pytest.mark.parametrize("two_launch", [0, 1])
+def test_split_grid_pass(lib, two_launch):
+    """K2 pass with more tiles than SMs: one split grid (full columns, then
+    z-chunk CTAs; default) or two launches (tuning key 6)."""
+    assert lib.sp_set_tuning(6, two_launch) == 0
+    dims = (700, 500, 40)   # 13 x 20 = 260 tiles at T=4 > 148 SMs
+    d0 = oracle.make_storage(*dims, init="random", seed=3, ring=0.5)
+    exp = oracle.interior(oracle.sweeps(d0, dims, 4), *dims)
+    g = sp.create_grid(*dims, init="random", seed=3, ring=0.5)
+    dst = g.copy()
+    sp.fused_sweeps(g, dst, 4)
+    assert_bitwise(dst.interior_numpy(), exp)
