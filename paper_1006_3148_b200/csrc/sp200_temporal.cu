@@ -1035,7 +1035,7 @@ static int dispatch_mirror(int levels, const LaunchReq &q) {
     default: {
         LaunchReq plain = q;
         plain.mirror = nullptr;
-        rc = (levels == 1 && tuning().cfg_index[1] != 0)
+        rc = (levels == 1 && tuning().cfg_index[1] >= 1 && tuning().cfg_index[1] <= 4)
                  ? launch_sweep1(q.src, q.dst, q.ex, q.ey, q.ez, q.nx, q.ny, q.nz, q.off, q.zlo, q.zhi,
                                  false, q.stream)
                  : dispatch(levels, plain);
@@ -1066,7 +1066,13 @@ static int dispatch(int levels, const LaunchReq &q) {
     }
     const int idx = (int)tuning().cfg_index[levels];
     switch (levels) {
-    case 1: return launch_cfg<1, 32, 4, 4>(q);
+    case 1:
+        switch (idx) {
+        case 5: return launch_cfg<1, 32, 4, 6>(q);
+        case 6: return launch_cfg<1, 16, 2, 4>(q);
+        case 7: return launch_cfg<1, 32, 4, 3>(q);
+        default: return launch_cfg<1, 32, 4, 4>(q);
+        }
     case 2:
         switch (idx) {
         case 1: return launch_cfg<2, 32, 4, 4>(q);
@@ -1108,7 +1114,7 @@ int launch_temporal(const double *src, double *dst, int64_t ex, int64_t ey, int6
     // per SM, 8-16-plane z-chunks) unless the ring copy of reference_sweep is
     // fused in, which k_sweep1 does; tuning key 2 (levels 1, index 1-4)
     // selects the k_sweep1 variants for A/B
-    if (levels == 1 && (copy_ring || tuning().cfg_index[1] != 0))
+    if (levels == 1 && (copy_ring || (tuning().cfg_index[1] >= 1 && tuning().cfg_index[1] <= 4)))
         return launch_sweep1(src, dst, ex, ey, ez, nx, ny, nz, off, zlo, zhi, copy_ring, stream);
     if (copy_ring) return set_error(SP_EUNSUP, "ring copy is fused only into the plain sweep");
     return dispatch(levels, q);

@@ -27,7 +27,7 @@ def lib():
 
 @pytest.mark.parametrize("levels,idx", [(lv, i) for lv in (2, 3, 4) for i in range(6)] +
                          [(4, 6)] +                                   # WP: level 0 from the stage ring
-                         [(1, i) for i in range(5)])                  # 0: k_temporal<1>, 1-4: k_sweep1
+                         [(1, i) for i in range(8)])   # 0, 5-7: k_temporal<1> tiles; 1-4: k_sweep1
 def test_kernel_variants(lib, levels, idx):
     assert lib.sp_set_tuning(2, levels * 16 + idx) == 0
     for dims in SHAPES:
