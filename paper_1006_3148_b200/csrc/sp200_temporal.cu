@@ -132,10 +132,16 @@ __device__ __forceinline__ void stg2_stream(double *p, double a, double b) {
 // previous plane from the stage ring instead of keeping them in registers
 // (W0, 4R doubles per thread).  The prefetch distance drops to S-2 so the
 // previous plane's stage is not refilled while it is still read.
-template <int T, int CY, int R, int S, bool TMA, bool COMP, int CL, bool MIR = false, bool WP = false>
+//
+// RING (depth 1, two-grid): reference_sweep's _copy_ring (sp/kernel.py:85-96)
+// fused in: CTAs whose tile touches a domain face, and every CTA at the two z
+// faces, copy the shell cells of their box from the stage into dst.
+template <int T, int CY, int R, int S, bool TMA, bool COMP, int CL, bool MIR = false, bool WP = false,
+          bool RING = false>
 __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB)
     k_temporal(const TParams p, const __grid_constant__ CUtensorMap tmap) {
     using C = KCfg<T, CY, R, S>;
+    static_assert(!RING || (T == 1 && !COMP && CL == 1 && !MIR), "RING: plain two-grid sweeps only");
     static_assert(!WP || (TMA && S >= 4), "WP: TMA loader, at least 4 stages");
     constexpr int PD = WP ? S - 2 : S - 1;  // stage prefetch distance
     constexpr int SPX = C::SPX, C0 = C::C0, PLANE = C::PLANE, PLANE_AL = C::PLANE_AL,
@@ -243,6 +249,8 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     }
     // warps without ring cells skip the select
     const bool wint = !__any_sync(0xffffffffu, ringb != 0u);
+    [[maybe_unused]] const bool ring_tile =
+        RING && (x0 == 0 || y0 == 0 || x0 + p.ox >= p.nx || y0 + OYc >= p.ny);
 
     const int nload = (z1 - z0) + 2 * T;      // level-0 planes z0-T .. z1+T-1
     const int nsteps = (z1 - z0) + 3 * T - 1;  // level T emits plane z0+s-3T+1 at step s
@@ -510,6 +518,48 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
             else cp_async_commit();
         }
         const double *cur = stage + si * PLANE_AL;
+        if constexpr (RING) {
+            // the stage holds logical plane P0 over storage columns bxs.. and
+            // rows bys..; copy the shell cells of this tile's box [x0-1, x0+ox]
+            // x [y0-1, y0+OY] (neighbouring tiles write the same values)
+            const int P0 = z0 - T + s;
+            const bool zring = (P0 == -1 && z0 == 0) || (P0 == p.nz && z1 == p.nz);
+            const bool zmid = (P0 >= z0) && (P0 < z1);
+            constexpr int BX = 64 + 2, BY = OYc + 2;  // box: ox <= 64 columns, OY rows, + halo
+            double *drow = p.dst + (int64_t)(P0 + p.off) * pz;
+            auto put = [&](int gx, int gy) {
+                drow[(int64_t)(gy + p.off) * p.ex + gx + p.off] =
+                    cur[(gy - (bys - p.off)) * SPX + (gx - (bxs - p.off))];
+            };
+            if (s < nload && zring) {
+                // a z face: the whole box is shell
+                for (int q = tid; q < BX * BY; q += NT) {
+                    const int qy = q / BX, qx = q - qy * BX;
+                    const int gx = x0 - 1 + qx, gy = y0 - 1 + qy;
+                    if (qx > p.ox + 1 || gx < -1 || gx > p.nx || gy < -1 || gy > p.ny) continue;
+                    put(gx, gy);
+                }
+            } else if (s < nload && zmid && ring_tile) {
+                // interior plane: only the box's x = -1 / nx columns and
+                // y = -1 / ny rows (one pass of the CTA's threads)
+                for (int q = tid; q < 2 * BY + 2 * BX; q += NT) {
+                    int gx, gy;
+                    bool ok;
+                    if (q < 2 * BY) {
+                        const int side = q >= BY;
+                        gx = side ? p.nx : -1;
+                        gy = y0 - 1 + (q - side * BY);
+                        ok = gx >= x0 - 1 && gx <= x0 + p.ox;
+                    } else {
+                        const int q2 = q - 2 * BY, side = q2 >= BX, qx = q2 - side * BX;
+                        gy = side ? p.ny : -1;
+                        gx = x0 - 1 + qx;
+                        ok = qx <= p.ox + 1 && gy >= y0 - 1 && gy <= y0 + OYc;
+                    }
+                    if (ok && gx >= -1 && gx <= p.nx && gy >= -1 && gy <= p.ny) put(gx, gy);
+                }
+            }
+        }
         // WP: the previous plane's stage (the current one at s = 0: that
         // step's level-1 output plane is below the valid range anyway)
         const double *prv = (WP && s > 0) ? stage + (int)((gbase + s + S - 1) % S) * PLANE_AL : cur;
@@ -704,6 +754,7 @@ struct LaunchReq {
     cudaStream_t stream;
     double *mirror = nullptr;     // two-grid: peer grid receiving every stored plane
     int64_t mirror_zshift = 0;    // storage plane z of dst -> z + zshift of mirror
+    bool ring = false;            // depth 1: fused ring copy (reference_sweep)
 };
 
 template <int T, int CY, int CL = 1>
@@ -844,6 +895,11 @@ static int launch_cfg(const LaunchReq &q) {
     } else {
         kern = use_tma ? k_temporal<T, CY, R, S, true, false, 1, false, WP>
                        : k_temporal<T, CY, R, S, false, false, 1>;
+        if constexpr (T == 1 && !WP) {
+            if (q.ring)
+                kern = use_tma ? k_temporal<T, CY, R, S, true, false, 1, false, false, true>
+                               : k_temporal<T, CY, R, S, false, false, 1, false, false, true>;
+        }
     }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)C::SMEM);
@@ -1111,12 +1167,13 @@ int launch_temporal(const double *src, double *dst, int64_t ex, int64_t ey, int6
                     int64_t zhi, bool copy_ring, cudaStream_t stream) {
     LaunchReq q{src, dst, ex, ey, ez, nx, ny, nz, off, off, zlo, zhi, 0, nullptr, stream};
     // plain sweeps: the depth-1 instance of this kernel (lane pairs, 2 CTAs
-    // per SM, 8-16-plane z-chunks) unless the ring copy of reference_sweep is
-    // fused in, which k_sweep1 does; tuning key 2 (levels 1, index 1-4)
-    // selects the k_sweep1 variants for A/B
-    if (levels == 1 && (copy_ring || (tuning().cfg_index[1] >= 1 && tuning().cfg_index[1] <= 4)))
+    // per SM, ~12-plane z-chunks), with reference_sweep's ring copy fused in
+    // when asked; tuning key 2 (levels 1, index 1-4) selects the older
+    // k_sweep1 variants for A/B
+    if (levels == 1 && tuning().cfg_index[1] >= 1 && tuning().cfg_index[1] <= 4)
         return launch_sweep1(src, dst, ex, ey, ez, nx, ny, nz, off, zlo, zhi, copy_ring, stream);
-    if (copy_ring) return set_error(SP_EUNSUP, "ring copy is fused only into the plain sweep");
+    if (copy_ring && levels != 1) return set_error(SP_EUNSUP, "ring copy is fused only into the plain sweep");
+    q.ring = copy_ring;
     return dispatch(levels, q);
 }
 
