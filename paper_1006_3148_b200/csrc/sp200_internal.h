@@ -21,6 +21,7 @@ struct Tuning {
     int64_t debug = 0;
     int64_t signal_kernels = 0;  // sp_signal / sp_wait through kernels, not stream memory ops
     int64_t two_launch = 0;      // K2 split pass as two launches instead of one split grid
+    int64_t balanced_split = 0;  // K2 split pass: full column + equal piece per CTA (A/B)
 };
 Tuning &tuning();
 

@@ -55,6 +55,10 @@ struct TParams {
     // two-grid split launch: CTAs from `split` on cover tiles
     // [tile_base2, tile_base2+tile_count2) in z-chunks of zc2 planes
     int split, tile_base2, tile_count2, zc2;
+    // balanced split (piece > 0): grid = `split` CTAs; CTA c marches tile c's
+    // whole column, then piece c (`piece` planes) of the remaining tiles'
+    // columns laid end to end (tile-major), one unit per tile it touches
+    int piece;
     int zlo, zhi, zc;
     int doff;        // storage offset of logical 0 in the written frame
     int direction;   // K3: +1 forward (write shifted -T), -1 backward
@@ -208,18 +212,41 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
 
     uint32_t gbase = 0;  // stage loads issued by this CTA before the current unit
     for (int unit = 0;; ++unit) {
-    if (unit > 0) break;
     // one (tile, z-chunk) unit per CTA, tile-fastest so that concurrently
     // running CTAs cover neighbouring tiles at the same z range and the
     // overlapped halo reads hit L2
     const int cid = (int)(blockIdx.x / CL);
-    const bool second = !COMP && cid >= p.split;
-    const int ucid = second ? cid - p.split : cid;
-    const int tcount = second ? p.tile_count2 : p.tile_count, uzc = second ? p.zc2 : p.zc;
-    const int tile = (second ? p.tile_base2 : p.tile_base) + ucid % tcount;
-    const int chunk = ucid / tcount;
-    const int z0 = p.zlo + chunk * uzc;
-    const int z1 = min(z0 + uzc, p.zhi);
+    int tile, chunk, z0, z1;
+    if (COMP || CL > 1 || p.piece == 0) {
+        if (unit > 0) break;
+        const bool second = !COMP && cid >= p.split;
+        const int ucid = second ? cid - p.split : cid;
+        const int tcount = second ? p.tile_count2 : p.tile_count, uzc = second ? p.zc2 : p.zc;
+        tile = (second ? p.tile_base2 : p.tile_base) + ucid % tcount;
+        chunk = ucid / tcount;
+        z0 = p.zlo + chunk * uzc;
+        z1 = min(z0 + uzc, p.zhi);
+    } else {
+        chunk = 0;
+        if (unit == 0) {
+            tile = cid;
+            z0 = p.zlo;
+            z1 = p.zhi;
+        } else {
+            const int64_t depth = p.zhi - p.zlo;
+            const int64_t lo = (int64_t)cid * p.piece, total = (int64_t)p.tile_count2 * depth;
+            const int64_t t = lo / depth + (unit - 1);
+            const int64_t b = max(lo, t * depth);
+            const int64_t e = min(min(lo + p.piece, (t + 1) * depth), total);
+            if (b >= e) break;
+            tile = p.tile_base2 + (int)t;
+            z0 = p.zlo + (int)(b - t * depth);
+            z1 = p.zlo + (int)(e - t * depth);
+        }
+        // the previous unit's last step may still read the stages the
+        // preload below refills
+        if (unit > 0) __syncthreads();
+    }
     const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
     const int x0 = tx * p.ox, y0 = ty * OYc;
     // logical coords of this CTA's region (0, 0)
@@ -966,6 +993,7 @@ static int launch_cfg(const LaunchReq &q) {
     p.tile_count = p.ntiles;
     p.split = 0x7fffffff;
     p.tile_base2 = p.tile_count2 = p.zc2 = 0;
+    p.piece = 0;
     if (grid * CL > 0x7fffffff) return set_error(SP_EUNSUP, "grid too large");
 
     CUtensorMap tmap;
@@ -988,6 +1016,19 @@ static int launch_cfg(const LaunchReq &q) {
         // tiles at the same z at the same time (L2 catches the halos).
         const int full = (int)((p.ntiles / slots) * slots);
         const int rem = p.ntiles - full;
+        if (tuning().balanced_split && CL == 1 && rem > 0) {
+            // every CTA: one full column, then an equal piece of the rest
+            TParams a = p;
+            a.tile_base = 0;
+            a.tile_count = full;
+            a.split = full;
+            a.tile_base2 = full;
+            a.tile_count2 = rem;
+            a.piece = (int)(((int64_t)rem * depth + full - 1) / full);
+            launch_units<CL>(kern, full, C::NT, C::SMEM, q.stream, a, tmap);
+            count_launch();
+            return check_launch("k_temporal");
+        }
         if (!tuning().two_launch && rem > 0) {
             // one grid: the chunk CTAs follow the full-column CTAs in
             // blockIdx order, so each starts on the first SM that frees up

@@ -23,6 +23,7 @@ def lib():
     for t in range(1, 5):
         L.sp_set_tuning(2, t * 16)
     L.sp_set_tuning(6, 0)
+    L.sp_set_tuning(7, 0)
 
 
 @pytest.mark.parametrize("levels,idx", [(lv, i) for lv in (2, 3, 4) for i in range(6)] +
@@ -46,11 +47,14 @@ def test_kernel_variants(lib, levels, idx):
         assert np.all(got[:zlo] == -3.0) and np.all(got[zhi:] == -3.0)
 
 
-@pytest.mark.parametrize("two_launch", [0, 1])
-def test_split_grid_pass(lib, two_launch):
+@pytest.mark.parametrize("two_launch,balanced", [(0, 0), (1, 0), (0, 1)])
+def test_split_grid_pass(lib, two_launch, balanced):
     """K2 pass with more tiles than SMs: one split grid (full columns, then
-    z-chunk CTAs; default) or two launches (tuning key 6)."""
+    z-chunk CTAs; default), two launches (tuning key 6), or one column plus
+    an equal piece of the remaining columns per CTA, pieces crossing tile
+    boundaries (tuning key 7)."""
     assert lib.sp_set_tuning(6, two_launch) == 0
+    assert lib.sp_set_tuning(7, balanced) == 0
     dims = (700, 500, 40)   # 13 x 20 = 260 tiles at T=4 > 148 SMs
     d0 = oracle.make_storage(*dims, init="random", seed=3, ring=0.5)
     exp = oracle.interior(oracle.sweeps(d0, dims, 4), *dims)
