@@ -198,7 +198,9 @@ int sp_wait(const uint32_t *flag, uint32_t value, void *stream);
  * key 4: profiling knobs (only in builds with -DSP200_PROFILE_KNOBS=1)
  * key 5: sp_signal / sp_wait through kernels instead of stream memory ops
  * key 6: split K2 passes as two launches (full columns, then z-chunks)
- *        instead of one grid (A/B only) */
+ *        instead of one grid (A/B only)
+ * key 7: split K2 passes as one full column plus an equal piece of the
+ *        remaining columns per CTA (A/B only) */
 int sp_set_tuning(int key, int64_t value);
 
 /* Query: 1 if the TMA loader applies to a grid with row extent `ex`. */
