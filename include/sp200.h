@@ -200,7 +200,8 @@ int sp_wait(const uint32_t *flag, uint32_t value, void *stream);
  * key 6: split K2 passes as two launches (full columns, then z-chunks)
  *        instead of one grid (A/B only)
  * key 7: split K2 passes as one full column plus an equal piece of the
- *        remaining columns per CTA (A/B only) */
+ *        remaining columns per CTA (A/B only)
+ * key 8: z-chunk length of the remaining tiles in a split K2 pass (0 = model) */
 int sp_set_tuning(int key, int64_t value);
 
 /* Query: 1 if the TMA loader applies to a grid with row extent `ex`. */

@@ -297,6 +297,7 @@ int sp_set_tuning(int key, int64_t value) {
     case 5: t.signal_kernels = value; return SP_OK;
     case 6: t.two_launch = value; return SP_OK;
     case 7: t.balanced_split = value; return SP_OK;
+    case 8: t.zchunk2 = value; return SP_OK;
     case 2: {
         int lv = (int)(value / 16), idx = (int)(value % 16);
         if (lv < 1 || lv > SP_MAX_FUSED) return set_error(SP_EINVAL, "bad levels in tuning");

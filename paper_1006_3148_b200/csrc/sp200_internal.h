@@ -22,6 +22,7 @@ struct Tuning {
     int64_t signal_kernels = 0;  // sp_signal / sp_wait through kernels, not stream memory ops
     int64_t two_launch = 0;      // K2 split pass as two launches instead of one split grid
     int64_t balanced_split = 0;  // K2 split pass: full column + equal piece per CTA (A/B)
+    int64_t zchunk2 = 0;         // K2 split pass: z-chunk length of the remaining tiles (0 = model)
 };
 Tuning &tuning();
 

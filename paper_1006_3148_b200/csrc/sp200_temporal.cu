@@ -1040,7 +1040,8 @@ static int launch_cfg(const LaunchReq &q) {
             a.split = full;
             a.tile_base2 = full;
             a.tile_count2 = rem;
-            const int64_t zcb = pick_zchunk(depth, rem, slots, T);
+            const int64_t zcb = tuning().zchunk2 > 0 ? std::min<int64_t>(tuning().zchunk2, depth)
+                                                     : pick_zchunk(depth, rem, slots, T);
             a.zc2 = (int)zcb;
             const int64_t gb = (int64_t)rem * ((depth + zcb - 1) / zcb);
             launch_units<CL>(kern, full + gb, C::NT, C::SMEM, q.stream, a, tmap);
