@@ -63,3 +63,24 @@ def test_tuning_and_tma_query():
     assert L.sp_set_tuning(2, 1 * 16 + 0) == 0
     assert L.sp_set_tuning(99, 0) == _lib.SP_EINVAL
     assert L.sp_launch_count(0) >= 0
+    # A/B keys documented in include/sp200.h: accepted and reset to defaults
+    for key in (1, 5, 6, 7, 8):
+        assert L.sp_set_tuning(key, 1) == 0
+        assert L.sp_set_tuning(key, 0) == 0
+    assert L.sp_set_tuning(2, 0 * 16) == _lib.SP_EINVAL   # levels outside [1, 4]
+
+
+def test_sp200_tune_env_hook():
+    """SP200_TUNE applies tuning pairs when the library loads (A/B runs of
+    bench.py); a malformed pair fails loudly."""
+    import subprocess
+    import sys
+    code = ("import paper_1006_3148_b200._lib as l; l.load(); print('ok')")
+    env = dict(os.environ, SP200_TUNE="6=1,8=64")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       cwd=ROOT)
+    assert r.returncode == 0 and "ok" in r.stdout
+    env["SP200_TUNE"] = "99=1"
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       cwd=ROOT)
+    assert r.returncode != 0 and "SP200_TUNE" in r.stderr
