@@ -70,6 +70,31 @@ class Clocks:
         self.path = None
 
     def start(self):
+        # NVML in a thread (20 ms period, no process start-up inside a
+        # sub-second timed region); nvidia-smi -lms 100 as the fallback
+        self.nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            rows, stop = [], threading.Event()
+
+            def sample():
+                while not stop.is_set():
+                    try:
+                        rows.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                                     pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM),
+                                     pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
+                    except Exception:
+                        pass
+                    stop.wait(0.02)
+
+            th = threading.Thread(target=sample, daemon=True)
+            th.start()
+            self.nvml = (pynvml, rows, stop, th)
+            return
+        except Exception:
+            self.nvml = None
         try:
             fd, self.path = tempfile.mkstemp(suffix=".csv")
             os.close(fd)
@@ -81,6 +106,24 @@ class Clocks:
             self.proc = None
 
     def stop(self):
+        if self.nvml is not None:
+            pynvml, rows, stop, th = self.nvml
+            stop.set()
+            th.join(timeout=2)
+            try:
+                pynvml.nvmlShutdown()
+            except Exception:
+                pass
+            if not rows:
+                return None
+            bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            reasons = sorted({n for n, b in bits.items() for r in rows if r[2] & b})
+            return {"sm_mhz": statistics.median(r[0] for r in rows),
+                    "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
+                    "samples": len(rows), "source": "nvml, 20 ms"}
         if self.proc is None:
             return None
         time.sleep(0.15)
