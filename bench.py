@@ -56,7 +56,7 @@ def _dist():
 
 
 # ---------------------------------------------------------------------------
-# clocks sampler (nvidia-smi during the timed region)
+# clocks sampler (NVML thread during the timed region; nvidia-smi as the fallback)
 # ---------------------------------------------------------------------------
 
 class Clocks:
