@@ -1,0 +1,59 @@
+"""CPU: the bench.py driver contract that does not need a GPU.
+
+- `--impl reference` prints one JSON line with the contract keys, the
+  reference arm's own `cpu_baseline` and a zero-byte `e2e`;
+- our arm fails loudly without a CUDA device (no CPU fallback);
+- `plan_depths` splits a solve into fused passes of at most t sweeps."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+def _run(*extra, timeout=600):
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    return subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *extra],
+                          capture_output=True, text=True, timeout=timeout, env=env, cwd=ROOT)
+
+
+def test_reference_arm_json_line():
+    r = _run("--impl", "reference", "--steps", "1", "--warmup", "0", "--ref-sweeps-per-step", "1")
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference"
+    assert d["unit"] == "GLUP/s" and d["higher_is_better"] is True
+    assert d["dtype"] == "f64" and d["steps"] == 1 and d["n_gpus"] == 1
+    assert d["value"] > 0
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "port" and cb["value"] == d["value"] and cb["cores"] >= 1
+    assert d["e2e"] == {"value": d["value"], "unit": "GLUP/s",
+                        "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+
+
+def test_our_arm_fails_without_gpu():
+    r = _run("--steps", "1", "--warmup", "3", "--quick", "--no-cpu")
+    assert r.returncode != 0
+    assert not [l for l in r.stdout.splitlines() if l.startswith("{")]
+
+
+@pytest.mark.parametrize("total,t", [(100, 4), (100, 3), (7, 4), (1, 4), (64, 1), (10, 8)])
+def test_plan_depths(total, t):
+    p = bench.plan_depths(total, t)
+    assert sum(p) == total
+    assert all(1 <= d <= t for d in p)
+    assert len(p) == -(-total // t)
+    assert max(p) - min(p) <= 1
