@@ -3,6 +3,7 @@
 - `--impl reference` prints one JSON line with the contract keys, the
   reference arm's own `cpu_baseline` and a zero-byte `e2e`;
 - our arm fails loudly without a CUDA device (no CPU fallback);
+- under torchrun (N=2) only rank 0 runs and prints the reference arm;
 - `plan_depths` splits a solve into fused passes of at most t sweeps."""
 
 import json
@@ -57,3 +58,18 @@ def test_plan_depths(total, t):
     assert all(1 <= d <= t for d in p)
     assert len(p) == -(-total // t)
     assert max(p) - min(p) <= 1
+
+
+def test_reference_arm_under_torchrun_prints_once():
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                        "--master-port", "29533", os.path.join(ROOT, "bench.py"),
+                        "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0",
+                        "--ref-sweeps-per-step", "1"],
+                       capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
