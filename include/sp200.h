@@ -148,13 +148,16 @@ int sp_temporal(const double *src, double *dst, int64_t ex, int64_t ey, int64_t 
  * read region go through `workspace` (a band stash) and are copied into place
  * by a second kernel, so no inter-CTA ordering is needed.
  * sp_compressed_workspace() returns the workspace bytes for a pass over
- * `depth` = zhi - zlo planes.
+ * `depth` = zhi - zlo planes (the worst case over the tile layouts a launch
+ * may pick); sp_compressed returns SP_EINVAL when `workspace_bytes` is
+ * smaller than the layout of this launch needs.
  */
 int64_t sp_compressed_workspace(int64_t nx, int64_t ny, int64_t depth, int levels);
 int sp_compressed(double *data, int64_t ex, int64_t ey, int64_t ez,
                   int64_t nx, int64_t ny, int64_t nz, int64_t src_off, int direction,
                   int levels, int64_t zlo, int64_t zhi, void *workspace,
-                  const double *const faces[6], int side_mask, void *stream);
+                  int64_t workspace_bytes, const double *const faces[6], int side_mask,
+                  void *stream);
 
 /*
  * Fused pass with peer delivery (z-slab halo exchange over NVLink peer

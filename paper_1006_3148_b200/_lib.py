@@ -56,7 +56,7 @@ def _declare(L):
         "sp_write_faces": ([dp, i64, i64, i64, i64, i64, i64, i64, ctypes.POINTER(dp), i32, vp], i32),
         "sp_temporal": ([dp, dp, i64, i64, i64, i64, i64, i64, i64, i32, i64, i64, vp], i32),
         "sp_compressed_workspace": ([i64, i64, i64, i32], i64),
-        "sp_compressed": ([dp, i64, i64, i64, i64, i64, i64, i64, i32, i32, i64, i64, vp,
+        "sp_compressed": ([dp, i64, i64, i64, i64, i64, i64, i64, i32, i32, i64, i64, vp, i64,
                            ctypes.POINTER(dp), i32, vp], i32),
         "sp_set_tuning": ([i32, i64], i32),
         "sp_temporal_mirror": ([dp, dp, i64, i64, i64, i64, i64, i64, i64, i32, i64, i64, dp, i64, i64,
@@ -105,6 +105,21 @@ def check(rc: int, what: str = "") -> None:
     if rc == SP_ERANGE:
         raise IndexError(msg)
     raise Sp200Error(msg)
+
+
+# Ring-write epoch: bumped by every wrapper whose kernel may store Dirichlet
+# ring cells through a raw pointer (torch's tensor version counters do not see
+# those writes).  kernel.rings_equal caches verdicts under it.
+_ring_epoch = 0
+
+
+def rings_touched() -> None:
+    global _ring_epoch
+    _ring_epoch += 1
+
+
+def ring_epoch() -> int:
+    return _ring_epoch
 
 
 def launch_count(reset: bool = False) -> int:

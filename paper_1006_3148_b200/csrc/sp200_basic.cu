@@ -438,9 +438,9 @@ int sp_rings_equal(const double *a, const double *b, int64_t ex, int64_t ey, int
     if (!a || !b || !equal) return set_error(SP_EINVAL, "null argument");
     int rc = check_geom(ex, ey, ez, nx, ny, nz, off);
     if (rc) return rc;
-    static std::mutex mu;
-    static int *host_flag = nullptr, *dev_flag = nullptr;
-    std::lock_guard<std::mutex> lock(mu);
+    // one mapped flag per host thread: concurrent callers on other threads
+    // (and their streams) never share it, so no lock is needed
+    static thread_local int *host_flag = nullptr, *dev_flag = nullptr;
     if (!host_flag) {
         if (cudaHostAlloc(reinterpret_cast<void **>(&host_flag), sizeof(int), cudaHostAllocMapped) !=
                 cudaSuccess ||
@@ -547,9 +547,9 @@ int64_t sp_compressed_workspace(int64_t nx, int64_t ny, int64_t depth, int level
 
 int sp_compressed(double *data, int64_t ex, int64_t ey, int64_t ez, int64_t nx, int64_t ny,
                   int64_t nz, int64_t src_off, int direction, int levels, int64_t zlo,
-                  int64_t zhi, void *flags, const double *const faces[6], int side_mask,
-                  void *stream) {
-    if (!data || !flags) return set_error(SP_EINVAL, "null argument");
+                  int64_t zhi, void *workspace, int64_t workspace_bytes,
+                  const double *const faces[6], int side_mask, void *stream) {
+    if (!data || !workspace) return set_error(SP_EINVAL, "null argument");
     if (direction != 1 && direction != -1) return set_error(SP_EINVAL, "direction must be +1 or -1");
     if (levels < 1 || levels > SP_MAX_FUSED)
         return set_error(SP_EUNSUP, "levels %d outside [1, %d]", levels, SP_MAX_FUSED);
@@ -563,7 +563,7 @@ int sp_compressed(double *data, int64_t ex, int64_t ey, int64_t ez, int64_t nx, 
     if (zhi > nz) zhi = nz;
     if (zlo < zhi) {
         rc = launch_compressed(data, ex, ey, ez, nx, ny, nz, src_off, direction, levels, zlo, zhi,
-                               flags, as_stream(stream));
+                               workspace, workspace_bytes, as_stream(stream));
         if (rc) return rc;
     }
     if (faces && side_mask) return sp_write_faces(data, ex, ey, ez, nx, ny, nz, doff, faces,

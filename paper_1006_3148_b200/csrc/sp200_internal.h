@@ -6,6 +6,12 @@
 
 #include "../../include/sp200.h"
 
+// A/B-only kernel variants (the first K1 k_sweep1, alternative K2 tile
+// configurations behind tuning key 2): compiled only with -DSP200_AB=1
+#ifndef SP200_AB
+#define SP200_AB 0
+#endif
+
 namespace sp200 {
 
 // Per-thread error message + status helpers.
@@ -42,7 +48,7 @@ bool tma_eligible(const void *ptr, int64_t ex, int64_t ey);
 int64_t compressed_workspace(int64_t nx, int64_t ny, int64_t depth, int levels);
 int launch_compressed(double *data, int64_t ex, int64_t ey, int64_t ez, int64_t nx, int64_t ny,
                       int64_t nz, int64_t src_off, int direction, int levels, int64_t zlo,
-                      int64_t zhi, void *ws, cudaStream_t stream);
+                      int64_t zhi, void *ws, int64_t ws_bytes, cudaStream_t stream);
 int launch_sweep1(const double *src, double *dst, int64_t ex, int64_t ey, int64_t ez,
                   int64_t nx, int64_t ny, int64_t nz, int64_t off, int64_t zlo, int64_t zhi,
                   bool copy_ring, cudaStream_t stream);

@@ -23,6 +23,8 @@
 //    every level; the valid output shrinks by one cell per side per level, so
 //    the stored tile is (CX-2(T-1)) x (CY-2(T-1)).  Cells outside the interior
 //    (Dirichlet ring) keep their input value at every level.
+#include "sp200_internal.h"
+#if SP200_AB  // A/B only: the first K1, superseded by the depth-1 k_temporal
 #include <string.h>
 
 #include <algorithm>
@@ -353,3 +355,5 @@ int launch_sweep1(const double *src, double *dst, int64_t ex, int64_t ey, int64_
 }
 
 }  // namespace sp200
+
+#endif  // SP200_AB

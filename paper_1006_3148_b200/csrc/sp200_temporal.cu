@@ -778,6 +778,7 @@ struct LaunchReq {
     int64_t ex, ey, ez, nx, ny, nz, off, doff, zlo, zhi;
     int direction;  // 0: two-grid (K1/K2); +1/-1: compressed in place (K3)
     void *ws;       // K3 workspace: the band stash
+    int64_t ws_bytes;
     cudaStream_t stream;
     double *mirror = nullptr;     // two-grid: peer grid receiving every stored plane
     int64_t mirror_zshift = 0;    // storage plane z of dst -> z + zshift of mirror
@@ -960,6 +961,10 @@ static int launch_cfg(const LaunchReq &q) {
     CompLayout L;
     if (comp) {
         comp_layout<T, CY>(q.nx, q.ny, q.zhi - q.zlo, q.off, aligned, &L);
+        const int64_t need = 8 * (L.nx_stash + L.ny_stash + L.nz_stash);
+        if (need > q.ws_bytes)
+            return set_error(SP_EINVAL, "compressed pass needs %lld workspace bytes, got %lld",
+                             (long long)need, (long long)q.ws_bytes);
         p.zc = (int)L.zc;
         grid = (int64_t)p.ntiles * L.nchunks;
         char *ws = reinterpret_cast<char *>(q.ws);
@@ -1133,10 +1138,14 @@ static int dispatch_mirror(int levels, const LaunchReq &q) {
     default: {
         LaunchReq plain = q;
         plain.mirror = nullptr;
+#if SP200_AB
         rc = (levels == 1 && tuning().cfg_index[1] >= 1 && tuning().cfg_index[1] <= 4)
                  ? launch_sweep1(q.src, q.dst, q.ex, q.ey, q.ez, q.nx, q.ny, q.nz, q.off, q.zlo, q.zhi,
                                  false, q.stream)
                  : dispatch(levels, plain);
+#else
+        rc = dispatch(levels, plain);
+#endif
         break;
     }
     }
@@ -1162,6 +1171,8 @@ static int dispatch(int levels, const LaunchReq &q) {
         default: return set_error(SP_EUNSUP, "levels %d unsupported", levels);
         }
     }
+#if SP200_AB
+    // A/B tile configurations (tuning key 2), built only with -DSP200_AB=1
     const int idx = (int)tuning().cfg_index[levels];
     switch (levels) {
     case 1:
@@ -1169,8 +1180,9 @@ static int dispatch(int levels, const LaunchReq &q) {
         case 5: return launch_cfg<1, 32, 4, 6>(q);
         case 6: return launch_cfg<1, 16, 2, 4>(q);
         case 7: return launch_cfg<1, 32, 4, 3>(q);
-        default: return launch_cfg<1, 32, 4, 4>(q);
+        default: break;
         }
+        break;
     case 2:
         switch (idx) {
         case 1: return launch_cfg<2, 32, 4, 4>(q);
@@ -1178,8 +1190,9 @@ static int dispatch(int levels, const LaunchReq &q) {
         case 3: return launch_cfg<2, 24, 2, 4>(q);
         case 4: return launch_cfg<2, 32, 4, 6, 2>(q);
         case 5: return launch_cfg<2, 32, 4, 6>(q);
-        default: return launch_cfg<2, 48, 4, 4>(q);  // 12 warps: 644 vs 602 GLUP/s (CY=32)
+        default: break;
         }
+        break;
     case 3:
         switch (idx) {
         case 1: return launch_cfg<3, 32, 4, 3>(q);
@@ -1187,8 +1200,9 @@ static int dispatch(int levels, const LaunchReq &q) {
         case 3: return launch_cfg<3, 24, 2, 4>(q);
         case 4: return launch_cfg<3, 32, 4, 5, 2>(q);
         case 5: return launch_cfg<3, 32, 4, 5>(q);
-        default: return launch_cfg<3, 36, 3, 4>(q);  // 12 warps: 727 vs 701 GLUP/s (CY=32)
+        default: break;
         }
+        break;
     case 4:
         switch (idx) {
         case 1: return launch_cfg<4, 32, 4, 3>(q);
@@ -1197,23 +1211,33 @@ static int dispatch(int levels, const LaunchReq &q) {
         case 4: return launch_cfg<4, 32, 4, 4, 2>(q);
         case 5: return launch_cfg<4, 36, 3, 4>(q);
         case 6: return launch_cfg<4, 32, 4, 5, 1, false, true>(q);  // WP: 735 vs 770 GLUP/s
-        default: return launch_cfg<4, 32, 4, 4>(q);  // 8 warps x 254 registers
+        default: break;
         }
-    default:
-        return set_error(SP_EUNSUP, "levels %d unsupported", levels);
+        break;
+    default: break;
+    }
+#endif
+    switch (levels) {
+    case 1: return launch_cfg<1, 32, 4, 4>(q);
+    case 2: return launch_cfg<2, 48, 4, 4>(q);  // 12 warps: 644 vs 602 GLUP/s (CY=32)
+    case 3: return launch_cfg<3, 36, 3, 4>(q);  // 12 warps: 727 vs 701 GLUP/s (CY=32)
+    case 4: return launch_cfg<4, 32, 4, 4>(q);  // 8 warps x 254 registers
+    default: return set_error(SP_EUNSUP, "levels %d unsupported", levels);
     }
 }
 
 int launch_temporal(const double *src, double *dst, int64_t ex, int64_t ey, int64_t ez,
                     int64_t nx, int64_t ny, int64_t nz, int64_t off, int levels, int64_t zlo,
                     int64_t zhi, bool copy_ring, cudaStream_t stream) {
-    LaunchReq q{src, dst, ex, ey, ez, nx, ny, nz, off, off, zlo, zhi, 0, nullptr, stream};
+    LaunchReq q{src, dst, ex, ey, ez, nx, ny, nz, off, off, zlo, zhi, 0, nullptr, 0, stream};
     // plain sweeps: the depth-1 instance of this kernel (lane pairs, 2 CTAs
     // per SM, ~12-plane z-chunks), with reference_sweep's ring copy fused in
     // when asked; tuning key 2 (levels 1, index 1-4) selects the older
     // k_sweep1 variants for A/B
+#if SP200_AB
     if (levels == 1 && tuning().cfg_index[1] >= 1 && tuning().cfg_index[1] <= 4)
         return launch_sweep1(src, dst, ex, ey, ez, nx, ny, nz, off, zlo, zhi, copy_ring, stream);
+#endif
     if (copy_ring && levels != 1) return set_error(SP_EUNSUP, "ring copy is fused only into the plain sweep");
     q.ring = copy_ring;
     return dispatch(levels, q);
@@ -1223,29 +1247,40 @@ int launch_temporal_mirror(const double *src, double *dst, int64_t ex, int64_t e
                            int64_t nx, int64_t ny, int64_t nz, int64_t off, int levels,
                            int64_t zlo, int64_t zhi, double *mirror, int64_t mirror_zshift,
                            cudaStream_t stream) {
-    LaunchReq q{src, dst, ex, ey, ez, nx, ny, nz, off, off, zlo, zhi, 0, nullptr, stream};
+    LaunchReq q{src, dst, ex, ey, ez, nx, ny, nz, off, off, zlo, zhi, 0, nullptr, 0, stream};
     q.mirror = mirror;
     q.mirror_zshift = mirror_zshift;
     return dispatch(levels, q);
 }
 
-int64_t compressed_workspace(int64_t nx, int64_t ny, int64_t depth, int levels) {
-    CompLayout L;
-    // off = levels gives par = 1: the narrower stored tile, i.e. the most bands
-    switch (levels) {
-    case 1: comp_layout<1, 32>(nx, ny, depth, 1, true, &L); break;
-    case 2: comp_layout<2, 32>(nx, ny, depth, 2, true, &L); break;
-    case 3: comp_layout<3, 32>(nx, ny, depth, 3, true, &L); break;
-    default: comp_layout<4, 32>(nx, ny, depth, 4, true, &L); break;
+// Worst case over the layouts a launch can pick: the stored-tile parity
+// (par 0 / 1, from the frame offset and the pointer alignment) changes the
+// tile count, and with it pick_zchunk's chunk count and all three stashes.
+template <int T>
+static int64_t comp_bytes_max(int64_t nx, int64_t ny, int64_t depth) {
+    int64_t best = 0;
+    for (int par = 0; par < 2; ++par) {
+        CompLayout L;
+        comp_layout<T, 32>(nx, ny, depth, (T - 1) + par, true, &L);
+        best = std::max(best, L.nx_stash + L.ny_stash + L.nz_stash);
     }
-    return 8 * (L.nx_stash + L.ny_stash + L.nz_stash) + 256;
+    return 8 * best + 256;
+}
+
+int64_t compressed_workspace(int64_t nx, int64_t ny, int64_t depth, int levels) {
+    switch (levels) {
+    case 1: return comp_bytes_max<1>(nx, ny, depth);
+    case 2: return comp_bytes_max<2>(nx, ny, depth);
+    case 3: return comp_bytes_max<3>(nx, ny, depth);
+    default: return comp_bytes_max<4>(nx, ny, depth);
+    }
 }
 
 int launch_compressed(double *data, int64_t ex, int64_t ey, int64_t ez, int64_t nx, int64_t ny,
                       int64_t nz, int64_t src_off, int direction, int levels, int64_t zlo,
-                      int64_t zhi, void *ws, cudaStream_t stream) {
+                      int64_t zhi, void *ws, int64_t ws_bytes, cudaStream_t stream) {
     const int64_t doff = src_off - (direction > 0 ? levels : -levels);
-    LaunchReq q{data, data, ex, ey, ez, nx, ny, nz, src_off, doff, zlo, zhi, direction, ws, stream};
+    LaunchReq q{data, data, ex, ey, ez, nx, ny, nz, src_off, doff, zlo, zhi, direction, ws, ws_bytes, stream};
     return dispatch(levels, q);
 }
 

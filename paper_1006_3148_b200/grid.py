@@ -63,6 +63,7 @@ class Grid3:
         if data is None:
             dev = _device(device)
             data = torch.empty(shape, dtype=torch.float64, device=dev)
+            _lib.rings_touched()
             _lib.check(_lib.load().sp_fill_constant(_ptr(data), data.numel(), 0.0, _stream()),
                        "Grid3")
         else:
@@ -122,6 +123,8 @@ class Grid3:
         g = Grid3(self.nx, self.ny, self.nz, self.pad, data=self.data.clone(),
                   alignment=self.alignment)
         g.boundary_faces = {k: v.clone() for k, v in self.boundary_faces.items()}
+        from .kernel import note_rings_equal
+        note_rings_equal(self, g)  # a clone's shell equals ours
         return g
 
     def checksum(self) -> str:
@@ -181,6 +184,7 @@ def fill_seeded(g: Grid3, seed: int, global_dims=None, global_origin=(0, 0, 0),
     138-143; sp/halo.py:132-147), every other stored cell = `shell`."""
     ex, ey, ez = g.extents
     gd = global_dims or g.shape
+    _lib.rings_touched()
     _lib.check(_lib.load().sp_fill_seeded(
         _ptr(g.data), ex, ey, ez, g.offset, g.nx, g.ny, g.nz,
         global_origin[0], global_origin[1], global_origin[2], gd[0], gd[1], gd[2],
@@ -204,6 +208,7 @@ def create_grid(nx, ny, nz, pad=0, init="constant", value=0.0, seed=0, *, ring=N
     g = Grid3(nx, ny, nz, pad, device=device)
     L = _lib.load()
     if init == "constant":
+        _lib.rings_touched()
         _lib.check(L.sp_fill_constant(_ptr(g.data), g.data.numel(), float(value), _stream()))
     elif init == "impulse":
         g.data[g.index(nx // 2, ny // 2, nz // 2)] = 1.0

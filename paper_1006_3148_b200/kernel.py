@@ -65,6 +65,7 @@ def apply_window(src: torch.Tensor, dst: torch.Tensor, window, src_off: int,
     if src.data_ptr() == dst.data_ptr() and src_off != dst_off:
         scratch = torch.empty((zh - zl) * (yh - yl) * (xh - xl), dtype=torch.float64,
                               device=src.device)
+    _lib.rings_touched()
     _lib.check(_lib.load().sp_apply_window(
         _ptr(src), _ptr(dst), ex, ey, ez, xl, xh, yl, yh, zl, zh, src_off, dst_off,
         _ptr(scratch) if scratch is not None else None, _stream()), "apply_window")
@@ -97,6 +98,7 @@ def write_faces(grid: Grid3, dst_off: int, side_mask: int = 63) -> None:
     for n, key in enumerate(FACE_KEYS):
         if (side_mask >> n) & 1 and grid.boundary_faces.get(key) is not None:
             mask |= 1 << n
+    _lib.rings_touched()
     _lib.check(_lib.load().sp_write_faces(
         _ptr(grid.data), ex, ey, ez, grid.nx, grid.ny, grid.nz, dst_off,
         ctypes.cast(faces, ctypes.POINTER(ctypes.c_void_p)), mask, _stream()), "write_faces")
@@ -105,8 +107,32 @@ def write_faces(grid: Grid3, dst_off: int, side_mask: int = 63) -> None:
 def copy_ring(a: Grid3, b: Grid3) -> None:
     """Copy the one-cell shell of A onto B (sp/kernel.py:85-96)."""
     ex, ey, ez = a.extents
+    _lib.rings_touched()
     _lib.check(_lib.load().sp_copy_ring(_ptr(a.data), _ptr(b.data), ex, ey, ez, a.nx, a.ny,
                                         a.nz, a.offset, _stream()), "copy_ring")
+    note_rings_equal(a, b)
+
+
+# Verdicts of rings_equal, keyed by both storages' pointers, frame offsets and
+# torch version counters plus the library's ring-write epoch: any write that
+# could change a shell (torch in-place ops, or an sp200 kernel that stores ring
+# cells) changes the key, so a cached verdict is never stale.  Calls that make
+# the shells equal by construction (copy_ring, reference_sweep, Grid3.copy)
+# record True without a device round trip.
+_RING_CACHE: dict = {}
+
+
+def _ring_key(a: Grid3, b: Grid3):
+    if a.data.data_ptr() > b.data.data_ptr():
+        a, b = b, a
+    return (a.data.data_ptr(), b.data.data_ptr(), a.offset, b.offset, tuple(a.data.shape),
+            tuple(b.data.shape), a.data._version, b.data._version, _lib.ring_epoch())
+
+
+def note_rings_equal(a: Grid3, b: Grid3) -> None:
+    if len(_RING_CACHE) > 256:
+        _RING_CACHE.clear()
+    _RING_CACHE[_ring_key(a, b)] = True
 
 
 def rings_equal(a: Grid3, b: Grid3) -> bool:
@@ -116,10 +142,16 @@ def rings_equal(a: Grid3, b: Grid3) -> bool:
     memory, not a copy engine)."""
     if a.data.shape != b.data.shape or a.offset != b.offset:
         return False
+    key = _ring_key(a, b)
+    if key in _RING_CACHE:
+        return _RING_CACHE[key]
     ex, ey, ez = a.extents
     eq = ctypes.c_int(0)
     _lib.check(_lib.load().sp_rings_equal(_ptr(a.data), _ptr(b.data), ex, ey, ez, a.nx, a.ny,
                                           a.nz, a.offset, ctypes.byref(eq), _stream()), "rings_equal")
+    if len(_RING_CACHE) > 256:
+        _RING_CACHE.clear()
+    _RING_CACHE[key] = bool(eq.value)
     return bool(eq.value)
 
 
@@ -135,8 +167,10 @@ def reference_sweep(a: Grid3, b: Grid3) -> None:
     if a.data.data_ptr() == b.data.data_ptr():
         raise ValueError("reference_sweep needs two distinct grids")
     ex, ey, ez = a.extents
+    _lib.rings_touched()
     _lib.check(_lib.load().sp_sweep(_ptr(a.data), _ptr(b.data), ex, ey, ez, a.nx, a.ny, a.nz,
                                     a.offset, 1, _stream()), "reference_sweep")
+    note_rings_equal(a, b)
 
 
 def spatial_blocked_sweep(a: Grid3, b: Grid3, spec: BlockSpec) -> None:
@@ -147,8 +181,10 @@ def spatial_blocked_sweep(a: Grid3, b: Grid3, spec: BlockSpec) -> None:
         raise ValueError(f"grid shapes differ: {a.shape} vs {b.shape}")
     spec.validate(a)
     ex, ey, ez = a.extents
+    _lib.rings_touched()
     _lib.check(_lib.load().sp_sweep(_ptr(a.data), _ptr(b.data), ex, ey, ez, a.nx, a.ny, a.nz,
                                     a.offset, 1, _stream()), "spatial_blocked_sweep")
+    note_rings_equal(a, b)
 
 
 def fused_sweeps(src: Grid3, dst: Grid3, levels: int, zlo: int = 0, zhi: int | None = None) -> None:
@@ -189,10 +225,11 @@ def compressed_pass(grid: Grid3, levels: int, direction: int, src_alignment: int
     for n, key in enumerate(FACE_KEYS):
         if (side_mask >> n) & 1 and grid.boundary_faces.get(key) is not None:
             mask |= 1 << n
+    _lib.rings_touched()
     _lib.check(_lib.load().sp_compressed(
         _ptr(grid.data), ex, ey, ez, grid.nx, grid.ny, grid.nz, grid.origin - src_alignment,
         int(direction), int(levels), int(zlo), int(grid.nz if zhi is None else zhi),
-        _ptr(workspace), ctypes.cast(faces, ctypes.POINTER(ctypes.c_void_p)), mask, _stream()),
+        _ptr(workspace), workspace.numel() * workspace.element_size(), ctypes.cast(faces, ctypes.POINTER(ctypes.c_void_p)), mask, _stream()),
         "compressed_pass")
 
 

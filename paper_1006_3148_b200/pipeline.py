@@ -315,6 +315,10 @@ class PipelineEngine:
                 lvl = L0 + u
                 src, dst = self.grids[(lvl - 1) % 2], self.grids[lvl % 2]
                 apply_window(src.data, dst.data, tuple(lives[u]), src.offset, src.offset)
+            if boundary is not None:
+                # the halo exchange is posted after the pass (run_pass contract)
+                dst = self.grids[(L0 + h) % 2]
+                boundary[2](dst.data, dst.offset)
             return h
         cur, other = self.grids[L0 % 2], self.grids[(L0 + 1) % 2]
         u0 = 0

@@ -86,3 +86,28 @@ def test_compressed_kernels_stay_in_bounds(t, dims):
     exp = oracle.interior(oracle.sweeps(oracle.make_storage(*dims, init="random", seed=3, lo=-1.0, hi=1.0),
                                         dims, 4 * t), *dims)
     assert_bitwise(g.interior_numpy(), exp)
+
+
+def test_compressed_workspace_covers_every_layout():
+    """sp_compressed_workspace is the worst case over the stored-tile parities
+    a launch may pick (the parity changes the tile count and so the z-chunk
+    count); a launch given less than its own layout needs fails with
+    ValueError instead of writing past the stash (512^3, t=1, pad 1: the case
+    where the parities pick different chunk counts)."""
+    n, t = 512, 1
+    bg, g = guarded_grid(n, n, n, pad=t, init="random", seed=9, lo=-1.0, hi=1.0)
+    nbytes = int(sp._lib.load().sp_compressed_workspace(n, n, n, t))
+    words = max(nbytes, 256) // 8 + 1
+    wbuf = torch.full((words + 2 * GUARD,), CANARY, dtype=torch.float64, device="cuda")
+    ws = wbuf[GUARD:GUARD + words].view(torch.uint8)
+    d = oracle.make_storage(n, n, n, pad=t, init="random", seed=9, lo=-1.0, hi=1.0)
+    with pytest.raises(ValueError):
+        compressed_pass(g, t, 1, g.alignment, ws[:64])
+    for direction in (1, -1):
+        compressed_pass(g, t, direction, g.alignment, ws)
+        g.alignment += t * direction
+    assert intact(bg, g.data.numel())
+    assert bool(torch.all(wbuf[:GUARD] == CANARY)) and bool(torch.all(wbuf[GUARD + words:] == CANARY))
+    a = oracle.make_storage(n, n, n, init="random", seed=9, lo=-1.0, hi=1.0)
+    exp = oracle.interior(oracle.sweeps(a, (n, n, n), 2), n, n, n)
+    assert_bitwise(g.interior_numpy(), exp)

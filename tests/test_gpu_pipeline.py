@@ -190,6 +190,41 @@ def test_unequal_rings_use_exact_per_level_path():
     assert_bitwise(st.result.interior_numpy(), oracle.interior(grids[3 % 2], n, n, n))
 
 
+def test_unfused_pass_still_posts_the_boundary():
+    """run_pass(direction, (lo, hi, post)): when the pass cannot fuse (here:
+    unequal rings), the per-level path must still call post once, after the
+    pass, with the grid holding the newest level (the halo exchange of the
+    z-slab drivers is posted only through it)."""
+    n = 16
+    d0 = oracle.make_storage(n, n, n, init="random", seed=4)
+    d1 = d0.copy()
+    d1[0, :, :] = 2.0
+    a = sp.Grid3.from_numpy(n, n, n, 0, d0)
+    b = sp.Grid3.from_numpy(n, n, n, 0, d1)
+    eng = sp.PipelineEngine(_cfg(spec=sp.BlockSpec(16, 4, 4), t=3), (a, b))
+    posted = []
+    eng.run_pass(1, (3, 3, lambda data, off: posted.append((data.data_ptr(), off))))
+    assert posted == [(eng.current_grid().data.data_ptr(), eng.current_grid().offset)]
+
+
+def test_rings_equal_cache_tracks_writes():
+    """rings_equal verdicts are cached per storage pair; copies that equalise
+    the shells record True without a device round trip, and any later write
+    (torch in-place ops, ring-writing kernels) invalidates the verdict."""
+    from paper_1006_3148_b200 import kernel
+    a = sp.create_grid(20, 18, 16, init="random", seed=1, ring=0.5)
+    b = a.copy()
+    assert kernel._ring_key(a, b) in kernel._RING_CACHE
+    assert sp.rings_equal(a, b)
+    b.data[0, 3, 3] = 7.0            # a z-low ring cell, through torch
+    assert not sp.rings_equal(a, b)
+    sp.copy_ring(a, b)
+    assert kernel._ring_key(a, b) in kernel._RING_CACHE and sp.rings_equal(a, b)
+    sp.kernel.write_faces(b, b.offset)  # kernel write: epoch bump, verdict recomputed
+    assert kernel._ring_key(a, b) not in kernel._RING_CACHE
+    assert sp.rings_equal(a, b)
+
+
 def test_large_config_c2_fused(golden):
     c = golden["configs"]["C2"]
     a = sp.create_grid(*c["n"], init="random", seed=c["seed"])
