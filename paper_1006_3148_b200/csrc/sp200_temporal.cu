@@ -66,6 +66,7 @@ struct TParams {
     double *mir;     // MIR: peer grid, pre-shifted so that mir + (g - dst) mirrors dst cell g
     int wx2, hy2;    // stash_x row width, stash_y rows per plane
     int debug;       // profiling only (sp_set_tuning key 4): 1 skip levels, 2 skip loads, 4 skip barrier
+    int c0;          // k_col: stage column of region column 0 (2 or 3: even TMA box start)
 };
 
 template <int T, int CY, int R, int S>
@@ -141,7 +142,7 @@ __device__ __forceinline__ void stg2_stream(double *p, double a, double b) {
 // fused in: CTAs whose tile touches a domain face, and every CTA at the two z
 // faces, copy the shell cells of their box from the stage into dst.
 template <int T, int CY, int R, int S, bool TMA, bool COMP, int CL, bool MIR = false, bool WP = false,
-          bool RING = false>
+          bool RING = false, bool XS1 = false>
 __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB)
     k_temporal(const TParams p, const __grid_constant__ CUtensorMap tmap) {
     using C = KCfg<T, CY, R, S>;
@@ -430,11 +431,21 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
             }
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                if (u == 1) {
+                if (u == 1 && !XS1) {
                     // level 0 lives in the stage: outer x-neighbours straight from
-                    // smem (shuffles here measured 636 vs 771 GLUP/s at T=4)
+                    // smem (two 4-way-conflicted LDS.64 per row)
                     xl[r] = B[(j0 + r + 1) * SPX + C0 + i0 - 1];
                     xr[r] = B[(j0 + r + 1) * SPX + C0 + i0 + 2];
+                } else if (u == 1) {
+                    // XS1: shuffles (2 MIO cycles per double, like one
+                    // conflict-free LDS.64), the region's outer columns -1 / 64
+                    // from the stage by the two edge lanes
+                    const bool edge = (lane == 0) || (lane == 31);
+                    const double e = edge ? B[(j0 + r + 1) * SPX + C0 + (lane == 0 ? -1 : 64)] : 0.0;
+                    const double up = __shfl_up_sync(0xffffffffu, A[r][1], 1);
+                    const double dn = __shfl_down_sync(0xffffffffu, A[r][0], 1);
+                    xl[r] = (lane == 0) ? e : up;
+                    xr[r] = (lane == 31) ? e : dn;
                 } else {
                     xl[r] = __shfl_up_sync(0xffffffffu, A[r][1], 1);
                     xr[r] = __shfl_down_sync(0xffffffffu, A[r][0], 1);
@@ -609,6 +620,275 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     // no CTA leaves while a peer may still address its shared memory
     if constexpr (CL > 1) cluster_sync_all();
 }
+
+
+#if SP200_AB
+// ---------------------------------------------------------------------------
+// K2 column layout (k_col): the two-grid fused pass with one column per lane.
+//
+// A warp spans the 32 columns of the region and lane l owns region column l
+// of R consecutive rows; NW warps stack in y (region 32 x NW*R).  Compared
+// with the lane-pair layout of k_temporal (64 x 4 per warp):
+//  * y-neighbours inside a thread's R = 8 rows are registers, so the
+//    published halo rows (first and last row of each warp, per level) and
+//    their loads are half as many per cell;
+//  * every shared-memory access is a warp-contiguous LDS.64 / STS.64
+//    (256 B, 2 wavefronts, no bank conflicts), where the pair layout's
+//    x-neighbour loads from the stage hit 4-way conflicts;
+//  * both x-neighbours of levels >= 2 come by shuffle (one each way per
+//    row); level 1 takes them from the stage (LDS) or, with XS, by shuffle
+//    with the two edge lanes patched from the stage;
+//  * stores are plain coalesced 8-byte stores (no pair alignment), so the
+//    stored tile keeps its full width 32 - 2(T-1) at every frame parity.
+// Shared memory traffic is the resource the pair layout saturates first
+// (l1tex 70 %, DESIGN.md §3 K2); this layout trades part of it for shuffles.
+// Same schedule, ring semantics and summation order as k_temporal.
+// ---------------------------------------------------------------------------
+template <int T, int R, int NW>
+struct CCfg {
+    static constexpr int CX = 32;
+    static constexpr int CY = NW * R;
+    static constexpr int SPX = CX + 4;                // stage row pitch = TMA box width
+    static constexpr int PY = CY + 2;
+    static constexpr int PLANE = SPX * PY;
+    static constexpr int PLANE_AL = (PLANE + 15) & ~15;
+    static constexpr int NT = 32 * NW;
+    static constexpr int OX = CX - 2 * (T - 1);
+    static constexpr int OY = CY - 2 * (T - 1);
+    static constexpr int PUBR = 2 * NW + 2;           // published rows per level plane (+2 sentinels)
+    static constexpr int PUB = PUBR * 32;
+    static constexpr int NPUB = (T > 1) ? 2 * (T - 1) : 0;
+    template <int S>
+    static constexpr size_t smem() {
+        return (size_t)S * PLANE_AL * 8 + (size_t)NPUB * PUB * 8 + 8 * S + 16;
+    }
+    static_assert(OY > 0 && OX > 0, "region too small for the fused depth");
+};
+
+template <int T, int R, int NW, int S, bool TMA, bool XS, bool MIR = false>
+__global__ void __launch_bounds__(32 * NW, 1)
+    k_col(const TParams p, const __grid_constant__ CUtensorMap tmap) {
+    using C = CCfg<T, R, NW>;
+    constexpr int SPX = C::SPX, PLANE = C::PLANE, PLANE_AL = C::PLANE_AL, NT = C::NT, PUB = C::PUB,
+                  OY = C::OY;
+    extern __shared__ __align__(128) double sm[];
+    double *stage = sm;
+    double *pub = sm + S * PLANE_AL;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(pub + C::NPUB * PUB);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int j0 = warp * R;  // first region row of this warp
+    if constexpr (TMA) {
+        if (tid == 0) {
+            tma_prefetch_desc(&tmap);
+#pragma unroll
+            for (int si = 0; si < S; ++si) mbar_init(&bar[si], 1);
+            fence_mbar_init();
+        }
+    }
+    // sentinel rows of the published planes (the halo of the region's first
+    // and last row: ghost cells, read but never feeding a kept cell)
+    for (int q = tid; q < C::NPUB * 64; q += NT)
+        pub[(q >> 6) * PUB + ((q & 32) ? (C::PUBR - 1) * 32 : 0) + (q & 31)] = 0.0;
+    __syncthreads();
+
+    // one (tile, z-chunk) unit per CTA, tile-fastest; CTAs from p.split on
+    // cover the remaining tiles in z-chunks (see launch_col)
+    const int cid = (int)blockIdx.x;
+    const bool second = cid >= p.split;
+    const int ucid = second ? cid - p.split : cid;
+    const int tcount = second ? p.tile_count2 : p.tile_count, uzc = second ? p.zc2 : p.zc;
+    const int tile = (second ? p.tile_base2 : p.tile_base) + ucid % tcount;
+    const int chunk = ucid / tcount;
+    const int z0 = p.zlo + chunk * uzc;
+    const int z1 = min(z0 + uzc, p.zhi);
+    const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
+    const int x0 = tx * p.ox, y0 = ty * OY;
+    const int rx0 = x0 - (T - 1), ry0 = y0 - (T - 1);  // logical coords of region (0, 0)
+    const int xc = rx0 + lane;
+
+    const bool col_ring = (xc == -1) || (xc == p.nx);
+    const bool x_out = (lane >= T - 1) && (lane < T - 1 + p.ox) && (xc < p.nx);
+    unsigned ringb = 0, yout = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int y = ry0 + j0 + r, jr = j0 + r;
+        if (col_ring || y == -1 || y == p.ny) ringb |= 1u << r;
+        if (jr >= T - 1 && jr < T - 1 + OY && y < p.ny) yout |= 1u << r;
+    }
+    const bool wint = !__any_sync(0xffffffffu, ringb != 0u);
+
+    const int nload = (z1 - z0) + 2 * T;       // level-0 planes z0-T .. z1+T-1
+    const int nsteps = (z1 - z0) + 3 * T - 1;  // level T emits plane z0+s-3T+1 at step s
+    const int c0 = p.c0;
+    const int bxs = rx0 + p.off - c0, bys = ry0 - 1 + p.off;
+    const int64_t pz = p.ex * p.ey;
+    double *dcol = p.dst + (int64_t)(ry0 + j0 + p.doff) * p.ex + (xc + p.doff);
+
+    auto issue = [&](int s) {
+        const int si = s % S;
+        const int zs = z0 - T + s + p.off;
+        if constexpr (TMA) {
+            mbar_arrive_expect_tx(&bar[si], PLANE * 8);
+            tma_load_3d(stage + si * PLANE_AL, &tmap, &bar[si], bxs, bys, zs);
+        } else {
+            double *dstage = stage + si * PLANE_AL;
+            const bool zok = (zs >= 0) && (zs < p.ez);
+            for (int q = tid; q < PLANE; q += NT) {
+                const int gx = bxs + q % SPX, gy = bys + q / SPX;
+                const bool inb = zok && gx >= 0 && gx < p.ex && gy >= 0 && gy < p.ey;
+                const double *g = inb ? p.src + ((int64_t)zs * p.ey + gy) * p.ex + gx : p.src;
+                cp_async_8(dstage + q, g, inb ? 8u : 0u);
+            }
+            cp_async_commit();
+        }
+    };
+    if constexpr (TMA) {
+        if (tid == 0)
+            for (int s = 0; s < S - 1; ++s)
+                if (s < nload) issue(s);
+    } else {
+        for (int s = 0; s < S - 1; ++s) {
+            if (s < nload) issue(s);
+            else cp_async_commit();
+        }
+    }
+
+    // per-thread state: pending sums of levels 1..T, level-0 own values and
+    // the outputs of levels 1..T-1, the last two by step parity
+    double Sp[T][R], W0[2][R], P[T > 1 ? T - 1 : 1][2][R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        W0[0][r] = W0[1][r] = 0.0;
+#pragma unroll
+        for (int u = 0; u < T; ++u) Sp[u][r] = 0.0;
+#pragma unroll
+        for (int u = 0; u < (T > 1 ? T - 1 : 1); ++u) P[u][0][r] = P[u][1][r] = 0.0;
+    }
+
+    // all levels advance one plane per step, deepest first; level u finishes
+    // plane z0 - T + s - 2u + 1 (MODE as in k_temporal)
+    auto levels = [&](int s, const double *cur, auto Qc, auto Mc) {
+        constexpr int Q = decltype(Qc)::value;
+        constexpr int MODE = decltype(Mc)::value;
+#pragma unroll
+        for (int u = T; u >= 1; --u) {
+            const int pout = z0 - T + s - 2 * u + 1;
+            const bool z_ring = (pout == -1) || (pout == p.nz);
+            double A[R], wl[R], xl[R], xr[R], cm, cp;
+            if (u == 1) {
+                const double *rp = cur + (j0 + 1) * SPX + c0 + lane;
+#pragma unroll
+                for (int r = 0; r < R; ++r) W0[Q][r] = rp[r * SPX];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    A[r] = W0[Q][r];
+                    wl[r] = W0[Q ^ 1][r];
+                }
+                cm = rp[-SPX];
+                cp = rp[R * SPX];
+                if constexpr (XS) {
+                    // edge lanes take the region's outer column from the stage
+                    const bool edge = (lane == 0) || (lane == 31);
+                    const double *ep = rp + (lane == 0 ? -1 : 1);
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const double e = edge ? ep[r * SPX] : 0.0;
+                        const double up = __shfl_up_sync(0xffffffffu, A[r], 1);
+                        const double dn = __shfl_down_sync(0xffffffffu, A[r], 1);
+                        xl[r] = (lane == 0) ? e : up;
+                        xr[r] = (lane == 31) ? e : dn;
+                    }
+                } else {
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        xl[r] = rp[r * SPX - 1];
+                        xr[r] = rp[r * SPX + 1];
+                    }
+                }
+            } else {
+                const int ui = (u > 1) ? u - 2 : 0;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    A[r] = P[ui][Q ^ 1][r];
+                    wl[r] = P[ui][Q][r];
+                }
+                const double *pp = pub + (ui * 2 + (Q ^ 1)) * PUB + lane;
+                cm = pp[(2 * warp) * 32];
+                cp = pp[(2 * warp + 3) * 32];
+                // lanes 0 / 31: the region's ghost columns, never feeding a kept cell
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    xl[r] = __shfl_up_sync(0xffffffffu, A[r], 1);
+                    xr[r] = __shfl_down_sync(0xffffffffu, A[r], 1);
+                }
+            }
+            double n[R], v[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[r] = dadd(Sp[u - 1][r], A[r]);
+#pragma unroll
+            for (int r = 0; r < R; ++r) n[r] = dadd(xl[r], xr[r]);
+#pragma unroll
+            for (int r = 0; r < R; ++r) n[r] = dadd(n[r], r == 0 ? cm : A[r > 0 ? r - 1 : 0]);
+#pragma unroll
+            for (int r = 0; r < R; ++r) n[r] = dadd(n[r], r == R - 1 ? cp : A[r < R - 1 ? r + 1 : 0]);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                v[r] = dmul(v[r], 1.0 / 6.0);
+                if constexpr (MODE == 1) {
+                    if (u < T && ((ringb >> r) & 1u)) v[r] = wl[r];
+                } else if constexpr (MODE == 2) {
+                    if (u < T && (((ringb >> r) & 1u) || z_ring)) v[r] = wl[r];
+                }
+                Sp[u - 1][r] = dadd(n[r], wl[r]);
+                if (u < T) P[u < T ? u - 1 : 0][Q][r] = v[r];
+            }
+            if (u < T) {
+                double *pw = pub + ((u - 1) * 2 + Q) * PUB + lane;
+                pw[(2 * warp + 1) * 32] = v[0];
+                pw[(2 * warp + 2) * 32] = v[R - 1];
+            } else if (x_out && pout >= z0 && pout < z1) {
+                double *g = dcol + (int64_t)(pout + p.doff) * pz;
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+                    if ((yout >> r) & 1u) {
+                        st_stream(g + (int64_t)r * p.ex, v[r]);
+                        if constexpr (MIR) st_stream(p.mir + (g - p.dst) + (int64_t)r * p.ex, v[r]);
+                    }
+            }
+        }
+    };
+
+    auto one_step = [&](int s, auto Qc) {
+        const int si = s % S;
+        if constexpr (TMA) {
+            if (s < nload) mbar_wait(&bar[si], (uint32_t)((s / S) & 1));
+        } else {
+            cp_async_wait<S - 2>();
+        }
+        __syncthreads();
+        if constexpr (TMA) {
+            if (tid == 0 && s + S - 1 < nload) issue(s + S - 1);
+        } else {
+            if (s + S - 1 < nload) issue(s + S - 1);
+            else cp_async_commit();
+        }
+        const double *cur = stage + si * PLANE_AL;
+        const int pmax = z0 - T + s - 1, pmin = z0 - T + s - 2 * T + 1;
+        const bool zall = (pmin >= 0) && (pmax < p.nz);
+        if (wint && zall) levels(s, cur, Qc, IC<0>{});
+        else if (zall) levels(s, cur, Qc, IC<1>{});
+        else levels(s, cur, Qc, IC<2>{});
+    };
+
+    for (int s = 0; s < nsteps; s += 2) {
+        one_step(s, IC<0>{});
+        if (s + 1 < nsteps) one_step(s + 1, IC<1>{});
+    }
+    if constexpr (!TMA) cp_async_wait<0>();
+}
+
+#endif  // SP200_AB
 
 struct UnstashArgs {
     double *data;
@@ -864,7 +1144,8 @@ static void comp_layout(int64_t nx, int64_t ny, int64_t depth, int64_t off, bool
     L->nz_stash = (L->nchunks - 1) * 2 * T * ny * ((nx + 2) & ~1);
 }
 
-template <int T, int CY, int R, int S, int CL = 1, bool MIRROR = false, bool WP = false>
+template <int T, int CY, int R, int S, int CL = 1, bool MIRROR = false, bool WP = false,
+          bool XS1 = false>
 static int launch_cfg(const LaunchReq &q) {
     using C = KCfg<T, CY, R, S>;
     const bool comp = q.direction != 0;
@@ -920,6 +1201,9 @@ static int launch_cfg(const LaunchReq &q) {
                        : k_temporal<T, CY, R, S, false, false, CL>;
     } else if (comp) {
         kern = use_tma ? k_temporal<T, CY, R, S, true, true, 1> : k_temporal<T, CY, R, S, false, true, 1>;
+    } else if constexpr (XS1) {
+        kern = use_tma ? k_temporal<T, CY, R, S, true, false, 1, false, false, false, true>
+                       : k_temporal<T, CY, R, S, false, false, 1, false, false, false, true>;
     } else {
         kern = use_tma ? k_temporal<T, CY, R, S, true, false, 1, false, WP>
                        : k_temporal<T, CY, R, S, false, false, 1>;
@@ -1116,6 +1400,113 @@ static int launch_cfg(const LaunchReq &q) {
     return rc;
 }
 
+
+#if SP200_AB
+// Host launch of k_col (two-grid passes, T = 2..4): same split schedule as
+// launch_cfg (full columns for one wave, the remaining tiles z-chunked).
+template <int T, int R, int NW, int S, bool XS, bool MIRROR = false>
+static int launch_col(const LaunchReq &q) {
+    using C = CCfg<T, R, NW>;
+    constexpr size_t SMEM = C::template smem<S>();
+    const bool use_tma = !tuning().force_cpasync && tma_eligible(q.src, q.ex, q.ey) && encode_fn();
+    TParams p;
+    memset(&p, 0, sizeof(p));
+    p.src = q.src;
+    p.dst = q.dst;
+    p.ex = q.ex;
+    p.ey = q.ey;
+    p.ez = q.ez;
+    p.nx = (int)q.nx;
+    p.ny = (int)q.ny;
+    p.nz = (int)q.nz;
+    p.off = (int)q.off;
+    p.doff = (int)q.doff;
+    p.ox = C::OX;
+    p.ex0 = T - 1;
+    p.tiles_x = (int)((q.nx + C::OX - 1) / C::OX);
+    p.tiles_y = (int)((q.ny + C::OY - 1) / C::OY);
+    p.ntiles = p.tiles_x * p.tiles_y;
+    p.zlo = (int)q.zlo;
+    p.zhi = (int)q.zhi;
+    // region column 0 sits at storage x = tx*OX - (T-1) + off (OX even), so
+    // c0 = 2 or 3 puts every tile's TMA box start on a 16-byte boundary
+    p.c0 = 2 + (int)((q.off - (T - 1)) & 1);
+    void (*kern)(const TParams, const CUtensorMap);
+    if constexpr (MIRROR) {
+        p.mir = q.mirror + q.mirror_zshift * q.ex * q.ey;
+        kern = use_tma ? k_col<T, R, NW, S, true, XS, true> : k_col<T, R, NW, S, false, XS, true>;
+    } else {
+        kern = use_tma ? k_col<T, R, NW, S, true, XS> : k_col<T, R, NW, S, false, XS>;
+    }
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    if (e != cudaSuccess) return set_error(SP_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::NT, SMEM);
+    if (occ < 1) occ = 1;
+    const int64_t slots = (int64_t)sm_count() * occ;
+    const int64_t depth = q.zhi - q.zlo;
+
+    CUtensorMap tmap;
+    memset(&tmap, 0, sizeof(tmap));
+    if (use_tma) {
+        cuuint64_t dims[3] = {(cuuint64_t)q.ex, (cuuint64_t)q.ey, (cuuint64_t)q.ez};
+        cuuint64_t strides[2] = {(cuuint64_t)(q.ex * 8), (cuuint64_t)(q.ex * q.ey * 8)};
+        cuuint32_t box[3] = {(cuuint32_t)C::SPX, (cuuint32_t)C::PY, 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        CUresult r = encode_fn()(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)q.src, dims,
+                                 strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return set_error(SP_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    }
+    p.tile_base = 0;
+    p.tile_count = p.ntiles;
+    p.split = 0x7fffffff;
+    int64_t grid;
+    if (tuning().zchunk <= 0 && p.ntiles >= slots) {
+        // one grid: `full` tiles march their whole column, the rest follow in
+        // blockIdx order as z-chunks sized to fill one more wave
+        const int full = (int)((p.ntiles / slots) * slots);
+        const int rem = p.ntiles - full;
+        p.tile_count = full;
+        p.zc = (int)depth;
+        if (rem > 0) {
+            p.split = full;
+            p.tile_base2 = full;
+            p.tile_count2 = rem;
+            const int64_t zcb = tuning().zchunk2 > 0 ? std::min<int64_t>(tuning().zchunk2, depth)
+                                                     : pick_zchunk(depth, rem, slots, T);
+            p.zc2 = (int)zcb;
+            grid = full + (int64_t)rem * ((depth + zcb - 1) / zcb);
+        } else {
+            grid = full;
+        }
+    } else {
+        int64_t zc = tuning().zchunk > 0 ? tuning().zchunk : pick_zchunk(depth, p.ntiles, slots, T);
+        if (zc < 1) zc = 1;
+        p.zc = (int)zc;
+        grid = (int64_t)p.ntiles * ((depth + zc - 1) / zc);
+    }
+    if (grid > 0x7fffffff) return set_error(SP_EUNSUP, "grid too large");
+    kern<<<(unsigned)grid, C::NT, SMEM, q.stream>>>(p, tmap);
+    count_launch();
+    return check_launch("k_col");
+}
+
+// two-grid K2 with the column layout (tuning key 9: 0 lane pairs, 1 columns
+// with level-1 x-neighbours from the stage, 2 columns with level-1 shuffles)
+template <bool MIRROR>
+static int dispatch_col(int levels, const LaunchReq &q, bool xs) {
+    switch (levels) {
+    case 2: return xs ? launch_col<2, 8, 12, 4, true, MIRROR>(q) : launch_col<2, 8, 12, 4, false, MIRROR>(q);
+    case 3: return xs ? launch_col<3, 6, 12, 4, true, MIRROR>(q) : launch_col<3, 6, 12, 4, false, MIRROR>(q);
+    case 4: return xs ? launch_col<4, 8, 8, 4, true, MIRROR>(q) : launch_col<4, 8, 8, 4, false, MIRROR>(q);
+    default: return set_error(SP_EUNSUP, "levels %d unsupported", levels);
+    }
+}
+
+#endif  // SP200_AB
+
 static int dispatch(int levels, const LaunchReq &q);
 
 static bool uses_tma(const LaunchReq &q) {
@@ -1160,6 +1551,20 @@ static int dispatch_mirror(int levels, const LaunchReq &q) {
 }
 
 static int dispatch(int levels, const LaunchReq &q) {
+#if SP200_AB
+    // A/B layouts (tuning key 9), DESIGN.md §8
+    if (q.direction == 0 && levels >= 2 && !q.mirror && tuning().k2_layout == 3) {
+        switch (levels) {
+        case 2: return launch_cfg<2, 48, 4, 4, 1, false, false, true>(q);
+        case 3: return launch_cfg<3, 36, 3, 4, 1, false, false, true>(q);
+        default: return launch_cfg<4, 32, 4, 4, 1, false, false, true>(q);
+        }
+    }
+    if (q.direction == 0 && levels >= 2 && !q.ring && tuning().k2_layout > 0 && tuning().k2_layout < 3) {
+        const bool xs = tuning().k2_layout == 2;
+        return q.mirror ? dispatch_col<true>(levels, q, xs) : dispatch_col<false>(levels, q, xs);
+    }
+#endif
     if (q.mirror) return dispatch_mirror(levels, q);
     if (q.direction != 0) {
         // K3: the CY = 32 instances, the geometry compressed_workspace sizes

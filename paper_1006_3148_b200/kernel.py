@@ -9,6 +9,7 @@ the results are bitwise identical to the reference sweep.
 from __future__ import annotations
 
 import ctypes
+import weakref
 
 import torch
 
@@ -125,14 +126,32 @@ _RING_CACHE: dict = {}
 def _ring_key(a: Grid3, b: Grid3):
     if a.data.data_ptr() > b.data.data_ptr():
         a, b = b, a
-    return (a.data.data_ptr(), b.data.data_ptr(), a.offset, b.offset, tuple(a.data.shape),
-            tuple(b.data.shape), a.data._version, b.data._version, _lib.ring_epoch())
+    return (id(a.data), id(b.data), a.data.data_ptr(), b.data.data_ptr(), a.offset, b.offset,
+            tuple(a.data.shape), tuple(b.data.shape), a.data._version, b.data._version,
+            _lib.ring_epoch())
+
+
+def _ring_lookup(a: Grid3, b: Grid3):
+    """Cached verdict, or None.  Entries hold weak references to both storage
+    tensors: a tensor freed and replaced by a new one at the same address
+    (the caching allocator reuses blocks) never matches an old entry."""
+    hit = _RING_CACHE.get(_ring_key(a, b))
+    if hit is None:
+        return None
+    wa, wb, verdict = hit
+    if {id(wa()), id(wb())} != {id(a.data), id(b.data)}:
+        return None
+    return verdict
+
+
+def _ring_store(a: Grid3, b: Grid3, verdict: bool) -> None:
+    if len(_RING_CACHE) > 256:
+        _RING_CACHE.clear()
+    _RING_CACHE[_ring_key(a, b)] = (weakref.ref(a.data), weakref.ref(b.data), verdict)
 
 
 def note_rings_equal(a: Grid3, b: Grid3) -> None:
-    if len(_RING_CACHE) > 256:
-        _RING_CACHE.clear()
-    _RING_CACHE[_ring_key(a, b)] = True
+    _ring_store(a, b, True)
 
 
 def rings_equal(a: Grid3, b: Grid3) -> bool:
@@ -142,16 +161,14 @@ def rings_equal(a: Grid3, b: Grid3) -> bool:
     memory, not a copy engine)."""
     if a.data.shape != b.data.shape or a.offset != b.offset:
         return False
-    key = _ring_key(a, b)
-    if key in _RING_CACHE:
-        return _RING_CACHE[key]
+    hit = _ring_lookup(a, b)
+    if hit is not None:
+        return hit
     ex, ey, ez = a.extents
     eq = ctypes.c_int(0)
     _lib.check(_lib.load().sp_rings_equal(_ptr(a.data), _ptr(b.data), ex, ey, ez, a.nx, a.ny,
                                           a.nz, a.offset, ctypes.byref(eq), _stream()), "rings_equal")
-    if len(_RING_CACHE) > 256:
-        _RING_CACHE.clear()
-    _RING_CACHE[key] = bool(eq.value)
+    _ring_store(a, b, bool(eq.value))
     return bool(eq.value)
 
 
