@@ -194,6 +194,25 @@ int sp_ipc_close(void *ptr);
 int sp_signal(uint32_t *flag, uint32_t value, void *stream);
 int sp_wait(const uint32_t *flag, uint32_t value, void *stream);
 
+/*
+ * Halo box pack / unpack for general Cartesian topologies (the strided
+ * message boxes of build_halo_plan, sp/halo.py:194-229, exchanged by
+ * exchange_multilayer_halos, sp/halo.py:239-271).  Box bounds are half-open
+ * STORAGE indices of `grid` (extents ex, ey, ez); `buf` is the box's
+ * contiguous (z, y, x)-ordered message buffer on the device.  One call
+ * handles up to SP_MAX_BOXES boxes (all messages of one axis phase): pack
+ * copies grid -> buf, unpack buf -> grid.
+ */
+#define SP_MAX_BOXES 8
+typedef struct {
+    int64_t x0, x1, y0, y1, z0, z1;
+    double *buf;
+} sp_box_t;
+int sp_pack_boxes(const double *grid, int64_t ex, int64_t ey, int64_t ez, int nbox,
+                  const sp_box_t *boxes, void *stream);
+int sp_unpack_boxes(double *grid, int64_t ex, int64_t ey, int64_t ez, int nbox,
+                    const sp_box_t *boxes, void *stream);
+
 /* Tuning knobs (benchmarking only; results never depend on them).
  * key 0: z-chunk length for sp_sweep / sp_temporal (0 = automatic)
  * key 1: force the cp.async (non-TMA) loader when nonzero

@@ -27,8 +27,16 @@ EXPORTS = (
     "sp_fill_constant", "sp_sweep", "sp_apply_window", "sp_window_gather",
     "sp_copy_ring", "sp_rings_equal", "sp_write_faces", "sp_temporal", "sp_compressed_workspace",
     "sp_compressed", "sp_set_tuning", "sp_tma_eligible", "sp_temporal_mirror", "sp_ipc_handle",
-    "sp_ipc_open", "sp_ipc_close", "sp_signal", "sp_wait",
+    "sp_ipc_open", "sp_ipc_close", "sp_signal", "sp_wait", "sp_pack_boxes", "sp_unpack_boxes",
 )
+SP_MAX_BOXES = 8
+
+
+class SpBox(ctypes.Structure):
+    """sp_box_t: half-open storage box + its contiguous device buffer."""
+    _fields_ = [("x0", ctypes.c_int64), ("x1", ctypes.c_int64), ("y0", ctypes.c_int64),
+                ("y1", ctypes.c_int64), ("z0", ctypes.c_int64), ("z1", ctypes.c_int64),
+                ("buf", ctypes.c_void_p)]
 
 _lib = None
 
@@ -67,6 +75,8 @@ def _declare(L):
         "sp_signal": ([vp, ctypes.c_uint32, vp], i32),
         "sp_wait": ([vp, ctypes.c_uint32, vp], i32),
         "sp_tma_eligible": ([i64, i64], i32),
+        "sp_pack_boxes": ([dp, i64, i64, i64, i32, ctypes.POINTER(SpBox), vp], i32),
+        "sp_unpack_boxes": ([dp, i64, i64, i64, i32, ctypes.POINTER(SpBox), vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

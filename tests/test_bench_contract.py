@@ -43,6 +43,18 @@ def test_reference_arm_json_line():
     assert cb["kind"] == "port" and cb["value"] == d["value"] and cb["cores"] >= 1
     assert d["e2e"] == {"value": d["value"], "unit": "GLUP/s",
                         "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    # same workload dict as our arm's N=1 line (BASELINE configs[1], C2)
+    assert d["config"] == bench.workload(1, False) and d["config"]["workload"].startswith("C2")
+    assert d["config"]["sweeps_per_step"] == 100
+    assert {"cpu_model", "os_cpu_count", "sched_getaffinity"} <= set(cb["host"])
+
+
+def test_workload_configs_name_baseline_configs():
+    w1, w2, w8 = bench.workload(1, False), bench.workload(2, True), bench.workload(8, True)
+    assert w1["grid"] == [512, 512, 512] and w1["sweeps_per_step"] == 100
+    assert w2["grid"] == [1024, 1024, 2048] and w8["grid"] == [1024, 1024, 8192]
+    assert w8["sweeps_per_step"] == 40 and w8["parallelism"] == "z-slab x8"
+    assert bench.C5["n"] == (2048, 2048, 2048) and bench.C5["ts"] == (1, 4, 8)
 
 
 def test_our_arm_fails_without_gpu():
@@ -73,3 +85,8 @@ def test_reference_arm_under_torchrun_prints_once():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    # N>1 measures BASELINE configs[3] (C4 weak scaling), the same config dict
+    # our arm prints, with the reference arm's own cpu_baseline and e2e
+    assert d["config"] == bench.workload(2, True)
+    assert d["config"]["workload"].startswith("C4") and d["config"]["grid"] == [1024, 1024, 2048]
+    assert d["cpu_baseline"]["kind"] == "port" and d["e2e"]["value"] == d["value"]

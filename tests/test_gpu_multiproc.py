@@ -33,7 +33,8 @@ def _worker(rank, world, port, case, out):
         torch.cuda.set_device(0)
         import paper_1006_3148_b200 as sp
         from paper_1006_3148_b200 import halo
-        cfg = sp.PipelineConfig(spec=sp.BlockSpec(8, 8, 8), t=case["h"], grid_mode=case["mode"])
+        cfg = sp.PipelineConfig(spec=sp.BlockSpec(*case.get("spec", (8, 8, 8))), t=case.get("t", case["h"]),
+                                T=case.get("T", 1), grid_mode=case["mode"])
         dc = halo.DistConfig(topo=halo.RankTopology(*case["topo"]), cfg=cfg, cycles=case["cycles"],
                              global_dims=tuple(case["global_dims"]), mode="strong", seed=case["seed"],
                              ring=case.get("ring"))
@@ -68,7 +69,17 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c['topo']}-h{c['h']}-{c['mode']}")
+# acceptance criterion #2 (pkg/tests/test_acceptance.py:94-158) over gloo:
+# the 12 topology / halo / mode cases at 60^3, seed 42, two cycles, each rank
+# a separate process with the GPU engine (the reference's in-process threads
+# plus its 2-rank TCP loopback run, in one matrix)
+for _topo in ((2, 1, 1), (2, 2, 1), (2, 2, 2)):
+    for _h, _mode in ((2, "two_grid"), (2, "compressed"), (4, "two_grid"), (4, "compressed")):
+        CASES.append(dict(topo=_topo, global_dims=(60, 60, 60), h=_h, t=2, T=1 if _h == 2 else 2,
+                          mode=_mode, cycles=2, seed=42, spec=(15, 10, 10)))
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c['topo']}-h{c['h']}-{c['mode']}-{c['global_dims'][0]}")
 def test_two_process_gpu_engine_equals_oracle(case, tmp_path):
     world = int(np.prod(case["topo"]))
     out = str(tmp_path / "full.npy")

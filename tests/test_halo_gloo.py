@@ -205,6 +205,43 @@ def test_distributed_equals_undecomposed_oracle(case, tmp_path):
         assert key in t
 
 
+def _owner_worker(rank, world, port, topo_dims, h, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        topo = halo.RankTopology(*topo_dims)
+        n_per = 12 if max(topo_dims) < 3 else 18
+        gd = tuple(n_per * p for p in topo_dims)
+        sub = halo.decompose_domain(gd, topo, halo.HaloSpec(h))[rank]
+        mx, my, mz = sub.local_dims
+        d = torch.zeros(oracle.storage_shape(mx, my, mz), dtype=torch.float64)
+        ob = sub.owned_box()
+        d[1 + ob[2][0]:1 + ob[2][1], 1 + ob[1][0]:1 + ob[1][1], 1 + ob[0][0]:1 + ob[0][1]] = float(rank)
+        halo.exchange_multilayer_halos(sub, halo.build_halo_plan(sub), data=d, offset=1)
+        gz = (sub.global_origin[2] + np.arange(mz))[:, None, None] // sub.owned[2]
+        gy = (sub.global_origin[1] + np.arange(my))[None, :, None] // sub.owned[1]
+        gx = (sub.global_origin[0] + np.arange(mx))[None, None, :] // sub.owned[0]
+        owner = (gx + topo.px * (gy + topo.py * gz)).astype(np.float64)
+        ok = np.array_equal(d.numpy()[1:1 + mz, 1:1 + my, 1:1 + mx], owner)
+        with open(f"{out}.{rank}", "w") as f:
+            f.write("ok" if ok else "bad")
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("topo_dims,h", [((2, 2, 2), 4), ((3, 2, 1), 1), ((2, 2, 1), 2)])
+def test_rank_id_fill_ownership_oracle_gloo(topo_dims, h, tmp_path):
+    """pkg/tests/test_halo.py:144-180 across processes: one exchange over
+    gloo and every halo cell (edges and corners by forwarding) holds its
+    owner's rank id."""
+    world = int(np.prod(topo_dims))
+    out = str(tmp_path / "owner")
+    mp.start_processes(_owner_worker, args=(world, _free_port(), topo_dims, h, out), nprocs=world,
+                       join=True, start_method="spawn")
+    assert all(open(f"{out}.{r}").read() == "ok" for r in range(world))
+
+
 def test_halo_plan_geometry_zslab():
     subs = halo.decompose_domain((64, 64, 96), halo.RankTopology(1, 1, 3), halo.HaloSpec(4))
     mid = subs[1]
