@@ -511,7 +511,8 @@ int sp_temporal(const double *src, double *dst, int64_t ex, int64_t ey, int64_t 
     if (src == dst) return set_error(SP_EINVAL, "sp_temporal: src and dst must differ");
     int rc = check_geom(ex, ey, ez, nx, ny, nz, off);
     if (rc) return rc;
-    if (levels < 1 || levels > SP_MAX_FUSED)
+    // A/B builds also carry deeper experimental instances (T = 5, 8)
+    if (levels < 1 || levels > (SP200_AB ? 8 : SP_MAX_FUSED))
         return set_error(SP_EUNSUP, "levels %d outside [1, %d]", levels, SP_MAX_FUSED);
     if (zlo < 0) zlo = 0;
     if (zhi > nz) zhi = nz;

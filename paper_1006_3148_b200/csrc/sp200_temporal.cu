@@ -1621,6 +1621,13 @@ static int dispatch(int levels, const LaunchReq &q) {
         break;
     default: break;
     }
+    // a deeper fused pass than SP_MAX_FUSED: the register state (3T doubles
+    // per cell) leaves T=5 at 2 rows x 2 columns per thread (12 warps, a
+    // 64 x 24 region, 1.71 executed LUP per LUP at 512^3): 535 vs 782 GLUP/s
+    // for T=4 (profiles/r02_ab_depth.log).  T=8 does not fit at all: 24
+    // doubles per cell of register state (R=4: 384 registers) and 14
+    // double-buffered level planes (333 KB of shared memory at CY=32).
+    if (levels == 5) return launch_cfg<5, 24, 2, 4>(q);
 #endif
     switch (levels) {
     case 1: return launch_cfg<1, 32, 4, 4>(q);
