@@ -218,6 +218,15 @@ def _cpu_child(target_s: float, n, max_sweeps: int, numpy_sweeps: int) -> int:
         dtn = time.perf_counter() - t1
         out["numpy"] = {"rate": n[0] * n[1] * n[2] * numpy_sweeps / dtn / 1e9, "sweeps": numpy_sweeps,
                         "dt": dtn}
+        # the reference's pipelined temporal blocking (run_pipelined with n=1,
+        # t=4, T=1, d_l=1, d_u=3, block (nx, 32, 32), relaxed sync): t threads
+        # running NumPy windows, one pass of 4 sweeps (oracle/pipelined.py)
+        from oracle.pipelined import pipelined_pass_two_grid
+        grids = [a, b]
+        t2 = time.perf_counter()
+        pipelined_pass_two_grid(grids, n, 4, (n[0], 32, 32))
+        dtp = time.perf_counter() - t2
+        out["pipelined"] = {"rate": n[0] * n[1] * n[2] * 4 / dtp / 1e9, "threads": 4, "dt": dtp}
     print(json.dumps(out))
     return 0
 
@@ -247,6 +256,13 @@ def cpu_rate(n, target_s: float = 12.0, max_sweeps: int = 100, numpy_sweeps: int
             "sample": (f"{r['numpy']['sweeps']} sweeps of the {g} grid through the oracle's NumPy "
                        f"restatement of reference_sweep (the reference's ufunc sequence, "
                        f"sp/kernel.py:51-58) in {r['numpy']['dt']:.1f} s")}
+    if "pipelined" in r:
+        cb["numpy_run_pipelined_t4"] = {
+            "value": r["pipelined"]["rate"], "unit": UNIT, "cores": r["pipelined"]["threads"],
+            "sample": (f"one pass of 4 sweeps of the {g} grid through the oracle's threaded NumPy "
+                       f"restatement of the reference's pipelined temporal blocking (run_pipelined with "
+                       f"n=1, t=4, T=1, d_l=1, d_u=3, block ({n[0]},32,32), relaxed sync; "
+                       f"sp/pipeline.py:363-395, 527-548) in {r['pipelined']['dt']:.1f} s")}
     return cb
 
 

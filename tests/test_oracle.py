@@ -107,3 +107,17 @@ def test_config_digests_c_oracle(golden, name):
     assert oracle.digest(oracle.interior(d0, *n, pad=c["pad"])) == c["init_digest"]
     out = oracle.c_sweeps(d0, d0.copy(), n, c["sweeps"], pad=c["pad"])
     assert oracle.digest(oracle.interior(out, *n, pad=c["pad"])) == c["digest"]
+
+
+@pytest.mark.parametrize("t,block,dims", [(4, (20, 6, 6), (20, 18, 24)), (2, (13, 5, 4), (13, 11, 9)),
+                                          (3, (8, 8, 8), (16, 16, 16))])
+def test_pipelined_restatement_equals_sweeps(t, block, dims):
+    """The threaded restatement of the reference's pipelined scheduler
+    (bench.py's second CPU baseline) equals t plain sweeps bit for bit."""
+    from oracle.pipelined import pipelined_pass_two_grid
+    d0 = oracle.make_storage(*dims, init="random", seed=3, ring=0.5)
+    grids = [d0.copy(), d0.copy()]
+    which = pipelined_pass_two_grid(grids, dims, t, block)
+    which = pipelined_pass_two_grid(grids, dims, t, block, levels_done=t)
+    exp = oracle.interior(oracle.sweeps(d0, dims, 2 * t), *dims)
+    assert np.array_equal(oracle.interior(grids[which], *dims), exp)
