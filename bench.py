@@ -559,13 +559,14 @@ def run_ours(args):
         redundancy = 1.0
     useful = value / ws * 6 / 1e3
     extra["compute_roofline"] = {
-        "bound": "mio (shared memory + shuffles)", "fp64_unit": "TFLOP/s (per GPU)",
+        "bound": "issue latency + LSU data pipe (not HBM, not FP64)", "fp64_unit": "TFLOP/s (per GPU)",
         "fp64_peak": fp64_peak, "fp64_achieved_useful": useful, "fp64_frac_useful": useful / fp64_peak,
         "executed_lup_per_lup": redundancy, "fp64_frac_executed": useful * redundancy / fp64_peak,
-        "note": ("6 DADD/DMUL per LUP, no FMA (bit-exact order). K2 T=4 is bound by the SM's MIO "
-                 "pipe: shared-memory wavefronts + SHFL.32 at 1 per clock per SM "
-                 "(tools/mio_bench.cu, profiles/r02_mio_bench.txt) about 80 % busy; FP64 pipe 38 %, "
-                 "issue 40 % (profiles/r01_s4_ncu_k2_t4_split.txt)")}
+        "note": ("6 DADD/DMUL per LUP, no FMA (bit-exact order). ncu K2 T=4 (profiles/r02_ncu_k2_t4.txt): "
+                 "LSU data pipe 68.5 % of peak (shared LD 64 M + ST 21 M + SHFL 37 M wavefronts per pass; "
+                 "SHFL.32 and LDS share that pipe at 1 wavefront per clock per SM, profiles/r02_mio_bench.txt), "
+                 "FP64 pipe 38 %, issue 40 % at 8 warps/SM (254 registers); top stalls: fixed-latency "
+                 "dependency 1.17, short scoreboard 0.80, barrier 0.53 per issue")}
 
     if rank == 0 and not slab and not args.quick:
         extra.update(_single_gpu_legs(sp, torch, bufs, peak, args))
