@@ -127,35 +127,53 @@ struct WinArgs {
     int64_t dex, dey, dxo, dyo, dzo;
 };
 
-__global__ void k_window(WinArgs a) {
-    const int64_t total = a.wx * a.wy * a.wz;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        int64_t ii = idx % a.wx;
-        int64_t r = idx / a.wx;
-        int64_t jj = r % a.wy;
-        int64_t kk = r / a.wy;
-        int64_t i = a.xl + ii, j = a.yl + jj, k = a.zl + kk;
-        const double *c = a.src + ((k + a.so) * a.ey + (j + a.so)) * a.ex + (i + a.so);
-        const int64_t py = a.ex, pz = a.ex * a.ey;
-        double v = stencil7(__ldg(c - 1), __ldg(c + 1), __ldg(c - py), __ldg(c + py),
-                            __ldg(c - pz), __ldg(c + pz));
-        a.dst[((kk + a.dzo) * a.dey + (jj + a.dyo)) * a.dex + (ii + a.dxo)] = v;
+// One thread per (x, y) column of the window, marching a z-chunk of WZC
+// planes: the z-neighbours rotate through registers (one new load per cell),
+// the x/y neighbours of the current plane come through L1 from the loads of
+// the adjacent threads, and the index math is 32-bit per thread, set up once.
+// Replaces the first version's one-thread-per-cell form (seven loads and a
+// 64-bit div/mod chain per cell).  Same summation order as every kernel.
+constexpr int WBX = 32, WBY = 8, WZC = 16;
+
+__global__ void __launch_bounds__(WBX * WBY) k_window(WinArgs a) {
+    const int ii = blockIdx.x * WBX + threadIdx.x, jj = blockIdx.y * WBY + threadIdx.y;
+    if (ii >= a.wx || jj >= a.wy) return;
+    const int kk0 = blockIdx.z * WZC;
+    const int kk1 = min((int64_t)kk0 + WZC, a.wz);
+    const int64_t py = a.ex, pz = a.ex * a.ey;
+    const double *c = a.src + ((a.zl + kk0 + a.so) * a.ey + (a.yl + jj + a.so)) * a.ex + (a.xl + ii + a.so);
+    double *d = a.dst + ((kk0 + a.dzo) * a.dey + (jj + a.dyo)) * a.dex + (ii + a.dxo);
+    const int64_t dpz = a.dex * a.dey;
+    double zm = __ldg(c - pz), z0 = __ldg(c);
+    for (int kk = kk0; kk < kk1; ++kk) {
+        const double zp = __ldg(c + pz);
+        *d = stencil7(__ldg(c - 1), __ldg(c + 1), __ldg(c - py), __ldg(c + py), zm, zp);
+        zm = z0;
+        z0 = zp;
+        c += pz;
+        d += dpz;
     }
 }
 
-// scratch (wz, wy, wx) -> dst frame
+static void launch_window(const WinArgs &a, cudaStream_t s) {
+    dim3 grid((unsigned)((a.wx + WBX - 1) / WBX), (unsigned)((a.wy + WBY - 1) / WBY),
+              (unsigned)((a.wz + WZC - 1) / WZC));
+    k_window<<<grid, dim3(WBX, WBY), 0, s>>>(a);
+}
+
+// scratch (wz, wy, wx) -> dst frame: one window row per CTA row (grid-stride
+// over the wy * wz rows), threads along x
 __global__ void k_unstage(const double *scratch, double *dst, int64_t ex, int64_t ey,
                           int64_t xo, int64_t yo, int64_t zo, int64_t wx, int64_t wy,
                           int64_t wz) {
-    const int64_t total = wx * wy * wz;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        int64_t ii = idx % wx;
-        int64_t r = idx / wx;
-        int64_t jj = r % wy;
-        int64_t kk = r / wy;
-        dst[((kk + zo) * ey + (jj + yo)) * ex + (ii + xo)] = scratch[idx];
+    const int64_t rows = wy * wz;
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+        const int64_t kk = r / wy, jj = r - kk * wy;
+        const double *s = scratch + r * wx;
+        double *d = dst + ((kk + zo) * ey + (jj + yo)) * ex + xo;
+        for (int64_t ii = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ii < wx;
+             ii += (int64_t)gridDim.x * blockDim.x)
+            d[ii] = s[ii];
     }
 }
 
@@ -385,12 +403,13 @@ int sp_apply_window(const double *src, double *dst, int64_t ex, int64_t ey, int6
         a.dzo = zl + dso;
     }
     cudaStream_t s = as_stream(stream);
-    const int64_t total = wx * wy * wz;
-    k_window<<<grid_for(total, 256), 256, 0, s>>>(a);
+    launch_window(a, s);
     count_launch();
     int rc = check_launch("sp_apply_window");
     if (rc || !alias) return rc;
-    k_unstage<<<grid_for(total, 256), 256, 0, s>>>(scratch, dst, ex, ey, xl + dso, yl + dso,
+    const int64_t urows = wy * wz;
+    dim3 ug((unsigned)((wx + 255) / 256), (unsigned)(urows < 65535 ? urows : 65535));
+    k_unstage<<<ug, 256, 0, s>>>(scratch, dst, ex, ey, xl + dso, yl + dso,
                                                    zl + dso, wx, wy, wz);
     count_launch();
     return check_launch("sp_apply_window(unstage)");
@@ -419,8 +438,7 @@ int sp_window_gather(const double *src, int64_t ex, int64_t ey, int64_t ez, int6
     a.dex = a.wx;
     a.dey = a.wy;
     a.dxo = a.dyo = a.dzo = 0;
-    const int64_t total = a.wx * a.wy * a.wz;
-    k_window<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(a);
+    launch_window(a, as_stream(stream));
     count_launch();
     return check_launch("sp_window_gather");
 }

@@ -133,12 +133,17 @@ def test_maximum_principle_and_linearity():
 
 
 def test_blocked_sweep_equals_reference():
-    for n, spec in ((6, (6, 6, 6)), (60, (60, 20, 20)), (7, (7, 3, 3))):
-        g = sp.create_grid(n, n, n, init="random", seed=4)
-        b1, b2 = g.copy(), g.copy()
-        sp.reference_sweep(g, b1)
+    """spatial_blocked_sweep (sp/kernel.py:114-125) against the oracle's
+    reference sweep, storage including the copied ring (tests/test_kernel.py:104-126)."""
+    import oracle
+    for n, spec in ((6, (6, 6, 6)), (60, (60, 20, 20)), (7, (7, 3, 3)), (33, (5, 7, 11))):
+        g = sp.create_grid(n, n, n, init="random", seed=4, ring=0.75)
+        b2 = sp.create_grid(n, n, n, init="constant", value=-2.0)
         sp.spatial_blocked_sweep(g, b2, sp.BlockSpec(*spec))
-        assert_bitwise(b2.interior_numpy(), b1.interior_numpy())
+        d0 = oracle.make_storage(n, n, n, init="random", seed=4, ring=0.75)
+        d1 = np.full_like(d0, -2.0)
+        oracle.reference_sweep(d0, d1, n, n, n, 1)
+        assert_bitwise(b2.to_numpy(), d1)
     with pytest.raises(ValueError):
         sp.spatial_blocked_sweep(g, b2, sp.BlockSpec(0, 1, 1))
 
