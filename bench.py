@@ -63,6 +63,14 @@ def workload(ws: int, slab: bool) -> dict:
             "l2_flush": "not needed: 17 GB per GPU working set > 126 MB L2"}
 
 
+def host_threads() -> int:
+    """Host threads this process may run on (the CPU baselines use all)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
 def host_info() -> dict:
     """Host CPU facts for the cpu_baseline."""
     model = platform.processor() or ""
@@ -236,9 +244,8 @@ def cpu_rate(n, target_s: float = 12.0, max_sweeps: int = 100, numpy_sweeps: int
     holds torch's thread pool, a CUDA context and the clock sampler; inside it
     the OpenMP sweep measured about half its rate).  Returns the cpu_baseline
     dict."""
-    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", ""))
-    if not env["OMP_NUM_THREADS"]:
-        env.pop("OMP_NUM_THREADS")
+    # every host core (torchrun exports OMP_NUM_THREADS=1 to each rank)
+    env = dict(os.environ, OMP_NUM_THREADS=str(host_threads()))
     # NumPy leg on one core: no BLAS threads (element-wise ufuncs are single-threaded anyway)
     out = subprocess.run([sys.executable, os.path.abspath(__file__), "--cpu-child", str(target_s),
                           "--cpu-n", ",".join(map(str, n)), "--cpu-numpy-sweeps", str(numpy_sweeps)],
@@ -288,7 +295,7 @@ def run_reference_arm(args):
         what = f"{sps} reference sweeps of the 512^3 C2 grid per step" + (
             " (the whole C2 solve)" if sps == C2["sweeps"] else "")
     a, b = d, d.copy()
-    threads = oracle.lib().or_max_threads()
+    threads = host_threads()  # all of them, whatever OMP_NUM_THREADS torchrun set
     for _ in range(args.warmup):
         oracle.c_sweeps(a, b, n, sps, threads=threads)
     t0 = time.perf_counter()
@@ -433,6 +440,8 @@ def run_ours(args):
     from paper_1006_3148_b200 import _lib
 
     ws, rank, local = _dist()
+    if args.dist_backend == "gloo":
+        local %= max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     slab = ws > 1 or args.slab
     if slab:
@@ -440,7 +449,11 @@ def run_ours(args):
         os.environ.setdefault("MASTER_PORT", "29533")
         os.environ.setdefault("RANK", "0")
         os.environ.setdefault("WORLD_SIZE", "1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            # path check only: several ranks on one GPU, halos staged through host memory
+            dist.init_process_group("gloo")
     L = _lib.load()
     peak, peak_src = _peaks()
 
@@ -845,6 +858,8 @@ def main():
     ap.add_argument("--cpu-numpy-sweeps", type=int, default=2, help=argparse.SUPPRESS)
     ap.add_argument("--ref-sweeps-per-step", type=int, default=0,
                     help="reference arm: sweeps per step (0 = the workload's, C2: 100; C4: 2-sweep sample)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help=argparse.SUPPRESS)  # gloo: N>1 path check with all ranks on one GPU
     ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
                     help="z-slab halo delivery for N>1: NCCL P2P, or the fused peer-memory stores")
     ap.add_argument("--slab", action="store_true",

@@ -90,3 +90,5 @@ def test_reference_arm_under_torchrun_prints_once():
     assert d["config"] == bench.workload(2, True)
     assert d["config"]["workload"].startswith("C4") and d["config"]["grid"] == [1024, 1024, 2048]
     assert d["cpu_baseline"]["kind"] == "port" and d["e2e"]["value"] == d["value"]
+    # torchrun exports OMP_NUM_THREADS=1; the reference arm still uses every host core
+    assert d["cpu_baseline"]["cores"] == len(os.sched_getaffinity(0))
