@@ -890,6 +890,276 @@ __global__ void __launch_bounds__(32 * NW, 1)
 
 #endif  // SP200_AB
 
+#if SP200_AB
+
+// ---------------------------------------------------------------------------
+// K2 with split level roles (k_split, T = 4): the pair layout of k_temporal
+// (lane = column pair x R=4 rows, 8 row groups of a 64 x 32 region), but two
+// warps per row group: a FRONT warp runs levels 1-2 and a BACK warp levels
+// 3-4 of the same cells.  The front warp hands its level-2 rows to the back
+// warp through a double-buffered shared plane, which also serves as the
+// level-2 halo rows (no separate level-2 publish).  Each thread keeps 5
+// doubles per cell instead of 12, so the CTA holds 16 warps (4 per
+// scheduler) at <= 128 registers, for 24 more shared-memory wavefronts per
+// row group and step (handoff store 16 + loads 24 - the level-2 publish 8 -
+// level-3 own values from registers ...).  Same schedule, level lag and
+// summation order as k_temporal (results are bit-identical).
+// ---------------------------------------------------------------------------
+template <int S, bool TMA>
+__global__ void __launch_bounds__(512, 1) k_split(const TParams p, const __grid_constant__ CUtensorMap tmap) {
+    constexpr int T = 4, CY = 32, R = 4, NWR = 8;  // levels, region rows, rows per thread, row groups
+    using C = KCfg<T, CY, R, S>;
+    constexpr int SPX = C::SPX, C0 = C::C0, PLANE = C::PLANE, PLANE_AL = C::PLANE_AL, NT = 512;
+    constexpr int OYc = CY - 2 * (T - 1);
+    extern __shared__ __align__(128) double sm[];
+    double *stage = sm;
+    double *pub1 = sm + S * PLANE_AL;         // level-1 boundary rows, 2 parities
+    double *hand = pub1 + 2 * PLANE_AL;       // level-2 rows (all), 2 parities
+    double *pub3 = hand + 2 * PLANE_AL;       // level-3 boundary rows, 2 parities
+    uint64_t *bar = reinterpret_cast<uint64_t *>(pub3 + 2 * PLANE_AL);
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const bool back = warp >= NWR;
+    const int wr = warp & (NWR - 1);
+    const int i0 = 2 * lane, j0 = wr * R;
+    if constexpr (TMA) {
+        if (tid == 0) {
+            tma_prefetch_desc(&tmap);
+#pragma unroll
+            for (int si = 0; si < S; ++si) mbar_init(&bar[si], 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+    }
+
+    const int cid = (int)blockIdx.x;
+    const bool second = cid >= p.split;
+    const int ucid = second ? cid - p.split : cid;
+    const int tcount = second ? p.tile_count2 : p.tile_count, uzc = second ? p.zc2 : p.zc;
+    const int tile = (second ? p.tile_base2 : p.tile_base) + ucid % tcount;
+    const int chunk = ucid / tcount;
+    const int z0 = p.zlo + chunk * uzc, z1 = min(z0 + uzc, p.zhi);
+    const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
+    const int x0 = tx * p.ox, y0 = ty * OYc;
+    const int rx0 = x0 - p.ex0, ry0 = y0 - (T - 1);
+
+    bool x_out[2];
+    unsigned ringb = 0;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const int xc = rx0 + i0 + c, ic = i0 + c;
+        x_out[c] = (ic >= p.ex0) && (ic < p.ex0 + p.ox) && (xc < p.nx);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int y = ry0 + j0 + r;
+            if (xc == -1 || xc == p.nx || y == -1 || y == p.ny) ringb |= 1u << (2 * r + c);
+        }
+    }
+    bool y_out[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int jr = j0 + r, y = ry0 + j0 + r;
+        y_out[r] = (jr >= T - 1) && (jr < T - 1 + OYc) && (y < p.ny);
+    }
+    const bool wint = !__any_sync(0xffffffffu, ringb != 0u);
+    const int nload = (z1 - z0) + 2 * T;
+    const int nsteps = (z1 - z0) + 3 * T - 1;
+    const int bxs = rx0 + p.off - C0, bys = ry0 - 1 + p.off;
+    const int64_t pz = p.ex * p.ey;
+    double *dcol = p.dst + (int64_t)(ry0 + j0 + p.doff) * p.ex + (rx0 + i0 + p.doff);
+
+    auto issue = [&](int s) {
+        const int si = s % S;
+        const int zs = z0 - T + s + p.off;
+        if constexpr (TMA) {
+            mbar_arrive_expect_tx(&bar[si], PLANE * 8);
+            tma_load_3d(stage + si * PLANE_AL, &tmap, &bar[si], bxs, bys, zs);
+        } else {
+            double *dstage = stage + si * PLANE_AL;
+            const bool zok = (zs >= 0) && (zs < p.ez);
+            for (int q = tid; q < PLANE; q += NT) {
+                const int gx = bxs + q % SPX, gy = bys + q / SPX;
+                const bool inb = zok && gx >= 0 && gx < p.ex && gy >= 0 && gy < p.ey;
+                const double *g = inb ? p.src + ((int64_t)zs * p.ey + gy) * p.ex + gx : p.src;
+                cp_async_8(dstage + q, g, inb ? 8u : 0u);
+            }
+            cp_async_commit();
+        }
+    };
+    if constexpr (TMA) {
+        if (tid == 0)
+            for (int s = 0; s < S - 1; ++s)
+                if (s < nload) issue(s);
+    } else {
+        for (int s = 0; s < S - 1; ++s) {
+            if (s < nload) issue(s);
+            else cp_async_commit();
+        }
+    }
+
+    // per-thread state: front = levels 1-2, back = levels 3-4
+    //   Spa/Spb: pending sums of the two levels; I[2]: the input level's own
+    //   values (front: level 0, back: level 2) by step parity; M[2]: the
+    //   middle level's outputs (front: level 1, back: level 3) by parity
+    double Spa[R][2], Spb[R][2], I[2][R][2], M[2][R][2];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) Spa[r][c] = Spb[r][c] = I[0][r][c] = I[1][r][c] = M[0][r][c] = M[1][r][c] = 0.0;
+
+    // One level of one role: input values A (own cells, this step's newest
+    // plane), wl (own cells, one plane older), halo rows cm / cp, x-neighbours
+    // by shuffle (or from `xrow` when the input is the stage).
+    auto level = [&](int u, double (&Sp)[R][2], double (&A)[R][2], double (&wl)[R][2], double2 cm,
+                     double2 cp, const double *xrow, auto Mc, double (&out)[R][2], int s) {
+        constexpr int MODE = decltype(Mc)::value;
+        const int pout = z0 - T + s - 2 * u + 1;
+        const bool z_ring = (pout == -1) || (pout == p.nz);
+        double xl[R], xr[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (xrow) {
+                xl[r] = xrow[r * SPX + C0 + i0 - 1];
+                xr[r] = xrow[r * SPX + C0 + i0 + 2];
+            } else {
+                xl[r] = __shfl_up_sync(0xffffffffu, A[r][1], 1);
+                xr[r] = __shfl_down_sync(0xffffffffu, A[r][0], 1);
+            }
+        }
+        double n[R][2], v[R][2];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) v[r][c] = dadd(Sp[r][c], A[r][c]);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            n[r][0] = dadd(xl[r], A[r][1]);
+            n[r][1] = dadd(A[r][0], xr[r]);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+                n[r][c] = dadd(n[r][c], (r == 0) ? (c ? cm.y : cm.x) : A[r > 0 ? r - 1 : 0][c]);
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+                n[r][c] = dadd(n[r][c], (r == R - 1) ? (c ? cp.y : cp.x) : A[r < R - 1 ? r + 1 : r][c]);
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                v[r][c] = dmul(v[r][c], 1.0 / 6.0);
+                if constexpr (MODE == 1) {
+                    if (u < T && ((ringb >> (2 * r + c)) & 1u)) v[r][c] = wl[r][c];
+                } else if constexpr (MODE == 2) {
+                    if (u < T && (((ringb >> (2 * r + c)) & 1u) || z_ring)) v[r][c] = wl[r][c];
+                }
+                Sp[r][c] = dadd(n[r][c], wl[r][c]);
+                out[r][c] = v[r][c];
+            }
+        return pout;
+    };
+
+    auto one_step = [&](int s, auto Qc) {
+        constexpr int Q = decltype(Qc)::value;
+        const int si = s % S;
+        if constexpr (TMA) {
+            if (s < nload) mbar_wait(&bar[si], (uint32_t)((s / S) & 1));
+        } else {
+            cp_async_wait<S - 2>();
+        }
+        __syncthreads();
+        if constexpr (TMA) {
+            if (tid == 0 && s + S - 1 < nload) issue(s + S - 1);
+        } else {
+            if (s + S - 1 < nload) issue(s + S - 1);
+            else cp_async_commit();
+        }
+        const double *cur = stage + si * PLANE_AL;
+        const int pmax = z0 - T + s - 1, pmin = z0 - T + s - 2 * T + 1;
+        const bool zall = (pmin >= 0) && (pmax < p.nz);
+        auto body = [&](auto Mc) {
+            if (!back) {
+                // level 2 from level 1 of the previous step (pub1[Q^1] halo rows)
+                {
+                    const double *B = pub1 + (Q ^ 1) * PLANE_AL;
+                    const double2 cm = lds2(B + j0 * SPX + C0 + i0), cp = lds2(B + (j0 + R + 1) * SPX + C0 + i0);
+                    double out[R][2];
+                    level(2, Spb, M[Q ^ 1], M[Q], cm, cp, nullptr, Mc, out, s);
+                    // hand all level-2 rows to the back warp (they are also its halo rows)
+                    double *H = hand + Q * PLANE_AL;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) sts2(H + (j0 + r + 1) * SPX + C0 + i0, out[r][0], out[r][1]);
+                }
+                // level 1 from the stage
+                {
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const double2 a = lds2(cur + (j0 + r + 1) * SPX + C0 + i0);
+                        I[Q][r][0] = a.x;
+                        I[Q][r][1] = a.y;
+                    }
+                    const double2 cm = lds2(cur + j0 * SPX + C0 + i0), cp = lds2(cur + (j0 + R + 1) * SPX + C0 + i0);
+                    level(1, Spa, I[Q], I[Q ^ 1], cm, cp, cur + (j0 + 1) * SPX, Mc, M[Q], s);
+                    double *W = pub1 + Q * PLANE_AL;
+                    sts2(W + (j0 + 1) * SPX + C0 + i0, M[Q][0][0], M[Q][0][1]);
+                    sts2(W + (j0 + R) * SPX + C0 + i0, M[Q][R - 1][0], M[Q][R - 1][1]);
+                }
+            } else {
+                // level 4 from level 3 of the previous step (pub3[Q^1] halo rows), stored
+                {
+                    const double *B = pub3 + (Q ^ 1) * PLANE_AL;
+                    const double2 cm = lds2(B + j0 * SPX + C0 + i0), cp = lds2(B + (j0 + R + 1) * SPX + C0 + i0);
+                    double out[R][2];
+                    const int pout = level(4, Spb, M[Q ^ 1], M[Q], cm, cp, nullptr, Mc, out, s);
+                    if (pout >= z0 && pout < z1) {
+#pragma unroll
+                        for (int r = 0; r < R; ++r) {
+                            if (!y_out[r]) continue;
+                            double *g = dcol + (int64_t)(pout + p.doff) * pz + (int64_t)r * p.ex;
+                            if (x_out[0] && x_out[1] && p.pair_store) {
+                                stg2_stream(g, out[r][0], out[r][1]);
+                            } else {
+                                if (x_out[0]) st_stream(g, out[r][0]);
+                                if (x_out[1]) st_stream(g + 1, out[r][1]);
+                            }
+                        }
+                    }
+                }
+                // level 3 from the front warp's level-2 rows of the previous step
+                {
+                    const double *H = hand + (Q ^ 1) * PLANE_AL;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const double2 a = lds2(H + (j0 + r + 1) * SPX + C0 + i0);
+                        I[Q][r][0] = a.x;
+                        I[Q][r][1] = a.y;
+                    }
+                    const double2 cm = lds2(H + j0 * SPX + C0 + i0), cp = lds2(H + (j0 + R + 1) * SPX + C0 + i0);
+                    level(3, Spa, I[Q], I[Q ^ 1], cm, cp, nullptr, Mc, M[Q], s);
+                    double *W = pub3 + Q * PLANE_AL;
+                    sts2(W + (j0 + 1) * SPX + C0 + i0, M[Q][0][0], M[Q][0][1]);
+                    sts2(W + (j0 + R) * SPX + C0 + i0, M[Q][R - 1][0], M[Q][R - 1][1]);
+                }
+            }
+        };
+        if (wint && zall) body(IC<0>{});
+        else if (zall) body(IC<1>{});
+        else body(IC<2>{});
+    };
+
+    for (int s = 0; s < nsteps; s += 2) {
+        one_step(s, IC<0>{});
+        if (s + 1 < nsteps) one_step(s + 1, IC<1>{});
+    }
+    if constexpr (!TMA) cp_async_wait<0>();
+}
+
+#endif  // SP200_AB
+
 struct UnstashArgs {
     double *data;
     int64_t ex, ey;
@@ -1402,6 +1672,81 @@ static int launch_cfg(const LaunchReq &q) {
 
 
 #if SP200_AB
+
+// Host launch of k_split (A/B: tuning key 9 = 4): the launch_cfg geometry of
+// the T=4 pair layout, 512 threads per CTA.
+template <int S>
+static int launch_split(const LaunchReq &q) {
+    using C = KCfg<4, 32, 4, S>;
+    constexpr size_t SMEM = (size_t)(S + 6) * C::PLANE_AL * 8 + 8 * S + 16;
+    const bool aligned =
+        ((reinterpret_cast<uintptr_t>(q.dst) | reinterpret_cast<uintptr_t>(q.src)) % 16 == 0) && (q.ex % 2 == 0);
+    TParams p;
+    memset(&p, 0, sizeof(p));
+    int tiles_y;
+    tile_geometry<4, 32>(q.nx, q.ny, q.off, aligned, &p.ox, &p.ex0, &p.tiles_x, &tiles_y);
+    const bool use_tma = aligned && !tuning().force_cpasync && tma_eligible(q.src, q.ex, q.ey) && encode_fn();
+    p.src = q.src;
+    p.dst = q.dst;
+    p.ex = q.ex;
+    p.ey = q.ey;
+    p.ez = q.ez;
+    p.nx = (int)q.nx;
+    p.ny = (int)q.ny;
+    p.nz = (int)q.nz;
+    p.off = (int)q.off;
+    p.doff = (int)q.doff;
+    p.pair_store = (aligned && ((q.off - q.doff) % 2 == 0)) ? 1 : 0;
+    p.tiles_y = tiles_y;
+    p.ntiles = p.tiles_x * tiles_y;
+    p.zlo = (int)q.zlo;
+    p.zhi = (int)q.zhi;
+    void (*kern)(const TParams, const CUtensorMap) = use_tma ? k_split<S, true> : k_split<S, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    if (e != cudaSuccess) return set_error(SP_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    const int64_t slots = sm_count();
+    const int64_t depth = q.zhi - q.zlo;
+    CUtensorMap tmap;
+    memset(&tmap, 0, sizeof(tmap));
+    if (use_tma) {
+        cuuint64_t dims[3] = {(cuuint64_t)q.ex, (cuuint64_t)q.ey, (cuuint64_t)q.ez};
+        cuuint64_t strides[2] = {(cuuint64_t)(q.ex * 8), (cuuint64_t)(q.ex * q.ey * 8)};
+        cuuint32_t box[3] = {(cuuint32_t)C::SPX, (cuuint32_t)C::PY, 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        CUresult r = encode_fn()(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)q.src, dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return set_error(SP_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    }
+    p.tile_base = 0;
+    p.tile_count = p.ntiles;
+    p.split = 0x7fffffff;
+    int64_t grid;
+    if (tuning().zchunk <= 0 && p.ntiles >= slots) {
+        const int full = (int)((p.ntiles / slots) * slots);
+        const int rem = p.ntiles - full;
+        p.tile_count = full;
+        p.zc = (int)depth;
+        grid = full;
+        if (rem > 0) {
+            p.split = full;
+            p.tile_base2 = full;
+            p.tile_count2 = rem;
+            const int64_t zcb = pick_zchunk(depth, rem, slots, 4);
+            p.zc2 = (int)zcb;
+            grid += (int64_t)rem * ((depth + zcb - 1) / zcb);
+        }
+    } else {
+        int64_t zc = tuning().zchunk > 0 ? tuning().zchunk : pick_zchunk(depth, p.ntiles, slots, 4);
+        if (zc < 1) zc = 1;
+        p.zc = (int)zc;
+        grid = (int64_t)p.ntiles * ((depth + zc - 1) / zc);
+    }
+    kern<<<(unsigned)grid, 512, SMEM, q.stream>>>(p, tmap);
+    count_launch();
+    return check_launch("k_split");
+}
+
 // Host launch of k_col (two-grid passes, T = 2..4): same split schedule as
 // launch_cfg (full columns for one wave, the remaining tiles z-chunked).
 template <int T, int R, int NW, int S, bool XS, bool MIRROR = false>
@@ -1553,6 +1898,7 @@ static int dispatch_mirror(int levels, const LaunchReq &q) {
 static int dispatch(int levels, const LaunchReq &q) {
 #if SP200_AB
     // A/B layouts (tuning key 9), DESIGN.md §8
+    if (q.direction == 0 && levels == 4 && !q.mirror && tuning().k2_layout == 4) return launch_split<4>(q);
     if (q.direction == 0 && levels >= 2 && !q.mirror && tuning().k2_layout == 3) {
         switch (levels) {
         case 2: return launch_cfg<2, 48, 4, 4, 1, false, false, true>(q);
