@@ -765,6 +765,34 @@ def _c5_strong(sp, torch, dist, ws, all_max):
     return out
 
 
+def _pcie_duplex(torch, host_in, host_out, dev, all_max) -> float:
+    """GB/s each way with an H2D and a D2H of one grid in flight together
+    (the e2e steady state), best of three; max over ranks of the time."""
+    a, b = torch.cuda.Stream(), torch.cuda.Stream()
+    scratch = torch.empty_like(dev)
+    best = None
+    for _ in range(3):
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        a.wait_event(e0)
+        b.wait_event(e0)
+        with torch.cuda.stream(a):
+            scratch.copy_(host_in, non_blocking=True)
+            ea = torch.cuda.Event(enable_timing=True)
+            ea.record(a)
+        with torch.cuda.stream(b):
+            host_out.copy_(dev, non_blocking=True)
+            eb = torch.cuda.Event(enable_timing=True)
+            eb.record(b)
+        torch.cuda.synchronize()
+        ms = max(e0.elapsed_time(ea), e0.elapsed_time(eb))
+        ms = all_max(ms)
+        best = ms if best is None else min(best, ms)
+    del scratch
+    return host_in.numel() * 8 / (best / 1e3) / 1e9
+
+
 def _e2e(sp, torch, dist, ws, slab, args, all_max, grid_bytes):
     """The same metric through the public API with host buffers (see
     e2e_pipelined): N=1 run_pipelined on C2; N>1 the z-slab driver on C4,
@@ -834,9 +862,18 @@ def _e2e(sp, torch, dist, ws, slab, args, all_max, grid_bytes):
     # the read-back must be the solve's result (last unit's grid)
     last = units[(steps - 1) % len(units)].result()
     assert torch.equal(host_out, last.cpu())
-    e2e = {"value": cells * sweeps / (ms / 1e3) / 1e9, "unit": UNIT,
+    pcie = _pcie_duplex(torch, host_in, host_out, last, all_max)
+    value = cells * sweeps / (ms / 1e3) / 1e9
+    # e2e roofline: one grid each way per step over this box's PCIe link with
+    # both directions busy (the solve hides under the transfers)
+    ceiling = cells * sweeps / (grid_bytes / (pcie * 1e9)) / 1e9
+    e2e = {"value": value, "unit": UNIT,
            "h2d_bytes_per_step": grid_bytes, "d2h_bytes_per_step": grid_bytes,
-           "ms_per_step": ms, "sweeps": sweeps, "pinned_host": pinned, "api": api}
+           "ms_per_step": ms, "sweeps": sweeps, "pinned_host": pinned, "api": api,
+           "roofline": {"bound": "pcie (H2D and D2H concurrently)", "link_gbs_each_way": pcie,
+                        "ceiling": ceiling, "frac": value / ceiling,
+                        "how": "one pinned grid H2D and one D2H at once on two streams, "
+                               "best of 3, measured on this box before the e2e leg's teardown"}}
     assert np.isfinite(e2e["value"])
     del units
     torch.cuda.empty_cache()
