@@ -66,3 +66,25 @@ def test_fused_live_z_range_random(nx, ny, nz, levels, data):
     if levels == 1:
         rest = rest[rest != -3.0]  # K1 writes whole planes of its range only
     assert np.all(rest == -3.0)
+
+
+@settings(max_examples=60, deadline=None, derandomize=True, suppress_health_check=[HealthCheck.too_slow])
+@given(topo=st.sampled_from([(1, 1, 2), (1, 1, 3), (1, 1, 4), (2, 1, 1), (1, 2, 1), (2, 2, 1), (2, 1, 2),
+                             (1, 2, 2), (2, 2, 2), (3, 1, 1), (1, 3, 2)]),
+       h=st.integers(1, 6), cycles=st.integers(1, 3), mode=st.sampled_from(["two_grid", "compressed"]),
+       ring=st.sampled_from([None, 0.5]), seed=st.integers(0, 1000), data=st.data())
+def test_distributed_random(topo, h, cycles, mode, ring, seed, data):
+    """run_distributed_inprocess on random topologies, halo widths, modes and
+    owned extents (ragged, down to the feasibility limit max(2(h-1), h)):
+    the assembled grid equals h * cycles undecomposed oracle sweeps."""
+    from paper_1006_3148_b200 import halo
+    lo = max(2 * (h - 1), h, 1)
+    owned = [data.draw(st.integers(lo if p > 1 else 1, lo + 9)) for p in topo]
+    gd = tuple(o * p for o, p in zip(owned, topo))
+    cfg = sp.PipelineConfig(spec=sp.BlockSpec(1, 1, 1), t=h,
+                            grid_mode=mode)
+    dc = halo.DistConfig(topo=halo.RankTopology(*topo), cfg=cfg, cycles=cycles, global_dims=gd,
+                         mode="strong", seed=seed, ring=ring)
+    g = halo.assemble_global(halo.run_distributed_inprocess(dc))
+    d0 = oracle.make_storage(*gd, init="random", seed=seed, ring=ring)
+    assert_bitwise(g.interior_numpy(), oracle.interior(oracle.sweeps(d0, gd, h * cycles), *gd))
