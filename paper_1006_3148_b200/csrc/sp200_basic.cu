@@ -317,7 +317,7 @@ int sp_set_tuning(int key, int64_t value) {
     case 7: t.balanced_split = value; return SP_OK;
     case 8: t.zchunk2 = value; return SP_OK;
     case 9:
-        if (value < 0 || value > 4) return set_error(SP_EINVAL, "k2 layout %lld outside [0, 4]", (long long)value);
+        if (value < 0 || value > 5) return set_error(SP_EINVAL, "k2 layout %lld outside [0, 5]", (long long)value);
         t.k2_layout = value;
         return SP_OK;
     case 2: {

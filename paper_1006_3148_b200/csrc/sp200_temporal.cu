@@ -142,13 +142,20 @@ __device__ __forceinline__ void stg2_stream(double *p, double a, double b) {
 // fused in: CTAs whose tile touches a domain face, and every CTA at the two z
 // faces, copy the shell cells of their box from the stage into dst.
 template <int T, int CY, int R, int S, bool TMA, bool COMP, int CL, bool MIR = false, bool WP = false,
-          bool RING = false, bool XS1 = false>
+          bool RING = false, bool XS1 = false, bool PS = false>
 __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB)
     k_temporal(const TParams p, const __grid_constant__ CUtensorMap tmap) {
     using C = KCfg<T, CY, R, S>;
     static_assert(!RING || (T == 1 && !COMP && CL == 1 && !MIR), "RING: plain two-grid sweeps only");
     static_assert(!WP || (TMA && S >= 4), "WP: TMA loader, at least 4 stages");
-    constexpr int PD = WP ? S - 2 : S - 1;  // stage prefetch distance
+    // PS (pair sync, A/B): no CTA-wide barrier per step.  Each warp syncs
+    // only with the warps above and below it (named barriers over 64
+    // threads; their halo rows are the only smem data warps share besides
+    // the stage), and the stage ring gets per-stage "empty" mbarriers that
+    // the TMA producer waits on, so a slow warp holds back its neighbours
+    // and, S - PD steps later, the producer, but not the whole CTA.
+    static_assert(!PS || (TMA && !COMP && CL == 1 && !RING && !WP && S >= 5), "PS: plain TMA two-grid passes");
+    constexpr int PD = WP ? S - 2 : (PS ? S - 3 : S - 1);  // stage prefetch distance
     constexpr int SPX = C::SPX, C0 = C::C0, PLANE = C::PLANE, PLANE_AL = C::PLANE_AL,
                   NT = C::NT;
     constexpr int NW = NT / 32;
@@ -185,6 +192,10 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
             if constexpr (TMA) tma_prefetch_desc(&tmap);
 #pragma unroll
             for (int si = 0; si < S; ++si) mbar_init(&bar[si], 1);
+            if constexpr (PS) {
+#pragma unroll
+                for (int si = 0; si < S; ++si) mbar_init(&bar[C::NBAR + si], NW);
+            }
             if constexpr (CL > 1) {
                 // arm phase 0 of every halo barrier: 64 doubles per row
 #pragma unroll
@@ -548,12 +559,30 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
         } else {
             cp_async_wait<S - 2>();
         }
+        if constexpr (PS) {
+            // even warps: upper pair first; odd warps: lower pair first, so
+            // all (2k, 2k+1) pairs complete together, then the (2k+1, 2k+2)
+            if (warp % 2 == 0) {
+                if (warp + 1 < NW) named_sync(warp + 1, 64);
+                if (warp > 0) named_sync(warp, 64);
+            } else {
+                named_sync(warp, 64);
+                if (warp + 1 < NW) named_sync(warp + 1, 64);
+            }
+            if (tid == 0 && s + PD < nload) {
+                const int t = s + PD;
+                // the stage's previous use (step t - S) released by every warp
+                if (t >= S) mbar_wait(&bar[C::NBAR + t % S], (uint32_t)(((t - S) / S) & 1));
+                issue(t);
+            }
+        } else {
         if (!(SP200_PROFILE_KNOBS && (p.debug & 4))) __syncthreads();
         if constexpr (TMA) {
             if (tid == 0 && s + PD < nload && !(SP200_PROFILE_KNOBS && (p.debug & 2))) issue(s + PD);
         } else {
             if (s + S - 1 < nload) issue(s + S - 1);
             else cp_async_commit();
+        }
         }
         const double *cur = stage + si * PLANE_AL;
         if constexpr (RING) {
@@ -608,6 +637,11 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
         if (wint && zall) levels(s, cur, prv, Qc, IC<0>{});
         else if (zall) levels(s, cur, prv, Qc, IC<1>{});
         else levels(s, cur, prv, Qc, IC<2>{});
+        if constexpr (PS) {
+            // this warp is done with the stage of step s
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar[C::NBAR + si]);
+        }
     };
 
     for (int s = 0; s < nsteps; s += 2) {
@@ -1415,9 +1449,10 @@ static void comp_layout(int64_t nx, int64_t ny, int64_t depth, int64_t off, bool
 }
 
 template <int T, int CY, int R, int S, int CL = 1, bool MIRROR = false, bool WP = false,
-          bool XS1 = false>
+          bool XS1 = false, bool PS = false>
 static int launch_cfg(const LaunchReq &q) {
     using C = KCfg<T, CY, R, S>;
+    constexpr size_t SMEM_B = C::SMEM + (PS ? 8 * S : 0);  // + the PS empty barriers
     const bool comp = q.direction != 0;
     if constexpr (CL > 1) {
         if (comp) return launch_cfg<T, CY, R, S, 1>(q);  // K3 runs unclustered
@@ -1471,6 +1506,9 @@ static int launch_cfg(const LaunchReq &q) {
                        : k_temporal<T, CY, R, S, false, false, CL>;
     } else if (comp) {
         kern = use_tma ? k_temporal<T, CY, R, S, true, true, 1> : k_temporal<T, CY, R, S, false, true, 1>;
+    } else if constexpr (PS) {
+        kern = use_tma ? k_temporal<T, CY, R, S, true, false, 1, false, false, false, false, true>
+                       : k_temporal<T, CY, R, S, false, false, 1>;
     } else if constexpr (XS1) {
         kern = use_tma ? k_temporal<T, CY, R, S, true, false, 1, false, false, false, true>
                        : k_temporal<T, CY, R, S, false, false, 1, false, false, false, true>;
@@ -1484,13 +1522,13 @@ static int launch_cfg(const LaunchReq &q) {
         }
     }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)C::SMEM);
+                                         (int)SMEM_B);
     if (e != cudaSuccess)
         return set_error(SP_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
 
     const int64_t depth = q.zhi - q.zlo;
     int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::NT, C::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::NT, SMEM_B);
     if (occ < 1) occ = 1;
     // concurrently resident units (tiles x chunks), CL CTAs each
     int64_t slots = (int64_t)sm_count() * occ / CL;
@@ -1498,7 +1536,7 @@ static int launch_cfg(const LaunchReq &q) {
         cudaLaunchConfig_t oc = {};
         oc.gridDim = dim3((unsigned)(slots * CL), 1, 1);
         oc.blockDim = dim3(C::NT, 1, 1);
-        oc.dynamicSmemBytes = C::SMEM;
+        oc.dynamicSmemBytes = SMEM_B;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
         at[0].val.clusterDim.x = CL;
@@ -1584,7 +1622,7 @@ static int launch_cfg(const LaunchReq &q) {
             a.tile_base2 = full;
             a.tile_count2 = rem;
             a.piece = (int)(((int64_t)rem * depth + full - 1) / full);
-            launch_units<CL>(kern, full, C::NT, C::SMEM, q.stream, a, tmap);
+            launch_units<CL>(kern, full, C::NT, SMEM_B, q.stream, a, tmap);
             count_launch();
             return check_launch("k_temporal");
         }
@@ -1603,7 +1641,7 @@ static int launch_cfg(const LaunchReq &q) {
                                                      : pick_zchunk(depth, rem, slots, T);
             a.zc2 = (int)zcb;
             const int64_t gb = (int64_t)rem * ((depth + zcb - 1) / zcb);
-            launch_units<CL>(kern, full + gb, C::NT, C::SMEM, q.stream, a, tmap);
+            launch_units<CL>(kern, full + gb, C::NT, SMEM_B, q.stream, a, tmap);
             count_launch();
             return check_launch("k_temporal");
         }
@@ -1611,7 +1649,7 @@ static int launch_cfg(const LaunchReq &q) {
         a.tile_base = 0;
         a.tile_count = full;
         a.zc = (int)depth;
-        launch_units<CL>(kern, full, C::NT, C::SMEM, q.stream, a, tmap);
+        launch_units<CL>(kern, full, C::NT, SMEM_B, q.stream, a, tmap);
         count_launch();
         int rc = check_launch("k_temporal");
         if (rc || rem == 0) return rc;
@@ -1621,11 +1659,11 @@ static int launch_cfg(const LaunchReq &q) {
         const int64_t zcb = pick_zchunk(depth, rem, slots, T);
         b.zc = (int)zcb;
         const int64_t gb = (int64_t)rem * ((depth + zcb - 1) / zcb);
-        launch_units<CL>(kern, gb, C::NT, C::SMEM, q.stream, b, tmap);
+        launch_units<CL>(kern, gb, C::NT, SMEM_B, q.stream, b, tmap);
         count_launch();
         return check_launch("k_temporal");
     }
-    launch_units<CL>(kern, grid, C::NT, C::SMEM, q.stream, p, tmap);
+    launch_units<CL>(kern, grid, C::NT, SMEM_B, q.stream, p, tmap);
     count_launch();
     int rc = check_launch("k_temporal");
     if (rc || !comp) return rc;
@@ -1899,6 +1937,13 @@ static int dispatch(int levels, const LaunchReq &q) {
 #if SP200_AB
     // A/B layouts (tuning key 9), DESIGN.md §8
     if (q.direction == 0 && levels == 4 && !q.mirror && tuning().k2_layout == 4) return launch_split<4>(q);
+    if (q.direction == 0 && levels >= 2 && !q.mirror && !q.ring && tuning().k2_layout == 5) {
+        switch (levels) {
+        case 2: return launch_cfg<2, 48, 4, 6, 1, false, false, false, true>(q);
+        case 3: return launch_cfg<3, 36, 3, 6, 1, false, false, false, true>(q);
+        default: return launch_cfg<4, 32, 4, 6, 1, false, false, false, true>(q);
+        }
+    }
     if (q.direction == 0 && levels >= 2 && !q.mirror && tuning().k2_layout == 3) {
         switch (levels) {
         case 2: return launch_cfg<2, 48, 4, 4, 1, false, false, true>(q);
