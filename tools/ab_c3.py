@@ -18,7 +18,9 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=600)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--zchunk", type=int, default=0)
+ap.add_argument("--maxfused", type=int, default=4, help="levels per K3 launch (a pass of 4 = 4/maxfused launches)")
 a = ap.parse_args()
+sp.PipelineEngine.max_fused = a.maxfused
 L = sp._lib.load()
 L.sp_set_tuning(0, a.zchunk)
 g = sp.create_grid(a.n, a.n, a.n, pad=4, init="random", seed=42, lo=-1.0, hi=1.0)
