@@ -705,6 +705,11 @@ def _single_gpu_legs(sp, torch, bufs, peak, args):
     ms4 = e0.elapsed_time(e1)
     extra["C4_single_gpu"] = {"glups": C4["n"][0] ** 3 * C4["sweeps"] / (ms4 / 1e3) / 1e9, "ms": ms4,
                               "config": "1024^3, ring 1.0, t=4, 40 sweeps (the per-GPU C4 block)"}
+    # the N>1 lines run C4 weak scaling: their per-GPU rate compares with this
+    # one-GPU C4 block, not with the C2 headline of this line
+    extra["weak_scaling_baseline"] = {"per_gpu_glups": extra["C4_single_gpu"]["glups"],
+                                      "workload": "C4 block at P=1 (1024^3, ring 1.0, t=4, 40 sweeps)",
+                                      "compare_with": "per_gpu_glups of the N>1 lines"}
     del a4, b4
     # C5 on one GPU: 2048^3 global, two 2050^3 grids = 137.8 GB of HBM,
     # 32 sweeps at t=1/4/8, device-timed with CUDA events
