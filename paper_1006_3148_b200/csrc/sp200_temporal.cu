@@ -67,7 +67,29 @@ struct TParams {
     int wx2, hy2;    // stash_x row width, stash_y rows per plane
     int debug;       // profiling only (sp_set_tuning key 4): 1 skip levels, 2 skip loads, 4 skip barrier
     int c0;          // k_col: stage column of region column 0 (2 or 3: even TMA box start)
+    // K3 DYN (A/B): band outputs go in place when the neighbour that reads
+    // them has already loaded that plane (its progress counter), else to
+    // the stash, flagged per (plane, tile) for the unstash kernels
+    int *progress;            // [ntiles] input planes fully loaded (+1), per launch
+    unsigned char *flag_y, *flag_x;  // [depth][ntiles]: band stashed at this output plane
 };
+
+// DYN launch order: tiles by anti-diagonal tx + ty, ascending for forward
+// passes (the lower neighbours that read a tile's bands start first),
+// descending for backward passes
+__device__ __forceinline__ int dyn_tile_of(int c, int tiles_x, int tiles_y, bool fwd) {
+    const int n = tiles_x * tiles_y;
+    if (!fwd) c = n - 1 - c;
+    for (int d = 0;; ++d) {
+        const int lo = max(0, d - (tiles_y - 1)), hi = min(d, tiles_x - 1);
+        const int cnt = hi - lo + 1;
+        if (c < cnt) {
+            const int tx = lo + c;
+            return (d - tx) * tiles_x + tx;
+        }
+        c -= cnt;
+    }
+}
 
 template <int T, int CY, int R, int S>
 struct KCfg {
@@ -142,7 +164,7 @@ __device__ __forceinline__ void stg2_stream(double *p, double a, double b) {
 // fused in: CTAs whose tile touches a domain face, and every CTA at the two z
 // faces, copy the shell cells of their box from the stage into dst.
 template <int T, int CY, int R, int S, bool TMA, bool COMP, int CL, bool MIR = false, bool WP = false,
-          bool RING = false, bool XS1 = false, bool PS = false>
+          bool RING = false, bool XS1 = false, bool PS = false, bool DYN = false>
 __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB)
     k_temporal(const TParams p, const __grid_constant__ CUtensorMap tmap) {
     using C = KCfg<T, CY, R, S>;
@@ -155,6 +177,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     // the TMA producer waits on, so a slow warp holds back its neighbours
     // and, S - PD steps later, the producer, but not the whole CTA.
     static_assert(!PS || (TMA && !COMP && CL == 1 && !RING && !WP && S >= 5), "PS: plain TMA two-grid passes");
+    static_assert(!DYN || COMP, "DYN: compressed passes only");
     constexpr int PD = WP ? S - 2 : (PS ? S - 3 : S - 1);  // stage prefetch distance
     constexpr int SPX = C::SPX, C0 = C::C0, PLANE = C::PLANE, PLANE_AL = C::PLANE_AL,
                   NT = C::NT;
@@ -196,6 +219,10 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
 #pragma unroll
                 for (int si = 0; si < S; ++si) mbar_init(&bar[C::NBAR + si], NW);
             }
+            if constexpr (DYN) {
+                reinterpret_cast<int *>(bar + C::NBAR)[0] = 0;  // stash everything until decided
+                reinterpret_cast<int *>(bar + C::NBAR)[1] = 0;
+            }
             if constexpr (CL > 1) {
                 // arm phase 0 of every halo barrier: 64 doubles per row
 #pragma unroll
@@ -236,6 +263,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
         const int tcount = second ? p.tile_count2 : p.tile_count, uzc = second ? p.zc2 : p.zc;
         tile = (second ? p.tile_base2 : p.tile_base) + ucid % tcount;
         chunk = ucid / tcount;
+        if constexpr (DYN) tile = dyn_tile_of(ucid, p.tiles_x, p.tiles_y, p.direction > 0);
         z0 = p.zlo + chunk * uzc;
         z1 = min(z0 + uzc, p.zhi);
     } else {
@@ -335,6 +363,17 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
         nrs = p.wx2;
     }
     const bool npair = x_out[0] && x_out[1] && (xband || p.pair_store);
+    // DYN: the tiles that read this tile's bands (forward: lower neighbours)
+    [[maybe_unused]] int rd_y = -1, rd_x = -1, rd_d = -1;
+    [[maybe_unused]] int c_y = 0x7fffffff, c_x = 0x7fffffff, c_d = 0x7fffffff;  // cached progress
+    [[maybe_unused]] double *icol = dcol + (int64_t)p.doff * pz;                // in-place column
+    if constexpr (DYN) {
+        const int dy = fwd ? -1 : 1, dx = fwd ? -1 : 1;
+        const bool hy = fwd ? ty > 0 : ty < p.tiles_y - 1, hx = fwd ? tx > 0 : tx < p.tiles_x - 1;
+        if (hy) { rd_y = tile + dy * p.tiles_x; c_y = -0x7fffffff; }
+        if (hx) { rd_x = tile + dx; c_x = -0x7fffffff; }
+        if (hx && hy) { rd_d = tile + dy * p.tiles_x + dx; c_d = -0x7fffffff; }
+    }
     double *sy_col = COMP ? p.stash_y + ((int64_t)ky0 - (int64_t)p.zlo * p.hy2) * srow + rx0 + i0 + sxpad
                           : nullptr;
     double *sz_col = COMP ? p.stash_z + (int64_t)(ry0 + j0) * srow + rx0 + i0 + sxpad : nullptr;
@@ -413,10 +452,17 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
             const bool store_plane = (u == T) && pout >= z0 && pout < z1;
             // K3 destinations of this level-T plane
             [[maybe_unused]] double *nrow = nullptr, *yrow = nullptr, *zrow = nullptr;
-            [[maybe_unused]] bool zb = false;
+            [[maybe_unused]] bool zb = false, dyn_yin = false, dyn_xin = false;
             if constexpr (COMP) {
                 if (u == T) {
                     nrow = ncol + (int64_t)pout * npz;
+                    if constexpr (DYN) {
+                        // the CTA-wide decision for this plane (thread 0, one
+                        // step earlier, published by the step barrier)
+                        const int w = reinterpret_cast<volatile int *>(bar + C::NBAR)[s & 1];
+                        dyn_yin = (w & 1) != 0;
+                        dyn_xin = (w & 2) != 0;
+                    }
                     const int zo = pout - z0;
                     zb = zband_chunk && (unsigned)(zo - zb_lo) < (unsigned)(2 * T);
                     zrow = sz_col + (int64_t)(zo + kz_off) * zstride;
@@ -520,7 +566,10 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
                         // in the same order); y and z bands are whole rows
                         double *row = nrow + (int64_t)r * nrs;
                         bool pr = npair;
-                        if (yb[r]) {
+                        if (DYN && ((yb[r] && dyn_yin) || (!yb[r] && xband && dyn_xin))) {
+                            row = icol + (int64_t)pout * pz + (int64_t)r * p.ex;
+                            pr = x_out[0] && x_out[1] && p.pair_store;
+                        } else if (yb[r]) {
                             row = yrow + (int64_t)r * srow;
                             pr = x_out[0] && x_out[1];
                         } else if (zb) {
@@ -547,6 +596,21 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
                             }
                         }
                     }
+                }
+            }
+            if constexpr (DYN) {
+                // flag the bands of this plane that went to the stash
+                if (u == T && store_plane && lane == 0) {
+                    bool any_y = false, any_n = false;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        if (!y_out[r]) continue;
+                        if (yb[r]) any_y = true;
+                        else any_n = true;
+                    }
+                    const int64_t fi = (int64_t)(pout - p.zlo) * p.ntiles + tile;
+                    if (any_y && !dyn_yin) p.flag_y[fi] = 1;
+                    if (any_n && rd_x >= 0 && !dyn_xin) p.flag_x[fi] = 1;
                 }
             }
         }
@@ -583,6 +647,25 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
             if (s + S - 1 < nload) issue(s + S - 1);
             else cp_async_commit();
         }
+        }
+        if constexpr (DYN) {
+            if (tid == 0) {
+                // every thread has waited for the stage of input plane z0-T+s:
+                // this tile no longer reads that plane from global memory
+                if (s < nload) st_relaxed_s32(p.progress + tile, z0 - T + s + 1);
+                // decide for the plane level T emits at step s+1: its band
+                // outputs overwrite input plane pout -/+ T, which every tile
+                // reading them must have loaded (forward: the lower x, y and
+                // diagonal neighbours; a y-band row also covers the corner
+                // columns the x neighbour reads)
+                const int pn = z0 - T + (s + 1) - 2 * T + 1;
+                const int need = (fwd ? pn - T : pn + T) + 1;
+                if (c_y < need) c_y = ld_acquire_s32(p.progress + rd_y);
+                if (c_x < need) c_x = ld_acquire_s32(p.progress + rd_x);
+                if (c_d < need) c_d = ld_acquire_s32(p.progress + rd_d);
+                const bool xi = c_x >= need, yi = xi && c_y >= need && c_d >= need;
+                reinterpret_cast<volatile int *>(bar + C::NBAR)[(s + 1) & 1] = (yi ? 1 : 0) | (xi ? 2 : 0);
+            }
         }
         const double *cur = stage + si * PLANE_AL;
         if constexpr (RING) {
@@ -1200,6 +1283,8 @@ struct UnstashArgs {
     int nx, ny, doff, zlo, zhi, zc, nchunks, ox, oy, tiles_x, tiles_y, T2, fwd, sxpad;
     const double *sx, *sy, *sz;
     int wx2, hy2;
+    const unsigned char *flag_y, *flag_x;  // DYN: per (plane, tile), null = copy all
+    int ntiles;
 };
 
 __device__ __forceinline__ bool band_hit(int v, int tile, int ntiles, int o, int T2, int fwd) {
@@ -1241,6 +1326,14 @@ __global__ void k_unstash_y(UnstashArgs a) {
     if (y >= a.ny) return;
     const double *src = a.sy + (int64_t)blockIdx.x * ((a.nx + 2) & ~1) + a.sxpad;
     double *dst = a.data + ((int64_t)(z + a.doff) * a.ey + (y + a.doff)) * a.ex + a.doff;
+    if (a.flag_y) {
+        // DYN: only the tiles whose band row of this plane went to the stash
+        const int bt = k / a.T2, ty = a.fwd ? bt + 1 : bt;
+        const unsigned char *f = a.flag_y + (int64_t)zr * a.ntiles + (int64_t)ty * a.tiles_x;
+        for (int x = threadIdx.x; x < a.nx; x += blockDim.x)
+            if (f[x / a.ox]) dst[x] = src[x];
+        return;
+    }
     copy_row_batched(dst, src, a.nx);
 }
 
@@ -1305,15 +1398,31 @@ __global__ void __launch_bounds__(64 * UXY) k_unstash_x(UnstashArgs a) {
         const bool ok1 = ok && xo + 1 >= 0 && xo + 1 < a.ox && x + 1 < a.nx;
         const bool pair = ok0 && ok1 && (((drow0 + x) & 1) == 0);
         if (!(ok0 || ok1)) continue;
+        unsigned lv = live;
+        if (a.flag_x) {
+            // DYN: rows whose tile kept this plane's x band in place are skipped
+            const int txb = a.fwd ? bt + 1 : bt;
+            int ty2 = y0 / a.oy, yo2 = y0 - ty2 * a.oy;
+#pragma unroll
+            for (int i = 0; i < UB; ++i) {
+                if (!a.flag_x[(int64_t)zr * a.ntiles + (int64_t)ty2 * a.tiles_x + txb]) lv &= ~(1u << i);
+                yo2 += UXY;
+                while (yo2 >= a.oy) {
+                    yo2 -= a.oy;
+                    ++ty2;
+                }
+                if (ty2 >= a.tiles_y) ty2 = a.tiles_y - 1;
+            }
+        }
         double2 v[UB];
 #pragma unroll
         for (int i = 0; i < UB; ++i)
-            v[i] = ((live >> i) & 1u)
+            v[i] = ((lv >> i) & 1u)
                        ? __ldcs(reinterpret_cast<const double2 *>(a.sx + srow0 + (int64_t)(UXY * i) * a.wx2 + c))
                        : make_double2(0.0, 0.0);
 #pragma unroll
         for (int i = 0; i < UB; ++i) {
-            if (!((live >> i) & 1u)) continue;
+            if (!((lv >> i) & 1u)) continue;
             double *d = a.data + drow0 + (int64_t)(UXY * i) * a.ex + x;
             if (pair) {
                 *reinterpret_cast<double2 *>(d) = v[i];
@@ -1449,7 +1558,7 @@ static void comp_layout(int64_t nx, int64_t ny, int64_t depth, int64_t off, bool
 }
 
 template <int T, int CY, int R, int S, int CL = 1, bool MIRROR = false, bool WP = false,
-          bool XS1 = false, bool PS = false>
+          bool XS1 = false, bool PS = false, bool DYN = false>
 static int launch_cfg(const LaunchReq &q) {
     using C = KCfg<T, CY, R, S>;
     constexpr size_t SMEM_B = C::SMEM + (PS ? 8 * S : 0);  // + the PS empty barriers
@@ -1487,6 +1596,8 @@ static int launch_cfg(const LaunchReq &q) {
     p.zlo = (int)q.zlo;
     p.zhi = (int)q.zhi;
     p.stash_x = p.stash_y = p.stash_z = nullptr;
+    p.progress = nullptr;
+    p.flag_y = p.flag_x = nullptr;
     p.debug = (int)tuning().debug;
     p.wx2 = p.hy2 = 0;
 
@@ -1505,7 +1616,11 @@ static int launch_cfg(const LaunchReq &q) {
         kern = use_tma ? k_temporal<T, CY, R, S, true, false, CL>
                        : k_temporal<T, CY, R, S, false, false, CL>;
     } else if (comp) {
-        kern = use_tma ? k_temporal<T, CY, R, S, true, true, 1> : k_temporal<T, CY, R, S, false, true, 1>;
+        if constexpr (DYN)
+            kern = use_tma ? k_temporal<T, CY, R, S, true, true, 1, false, false, false, false, false, true>
+                           : k_temporal<T, CY, R, S, false, true, 1, false, false, false, false, false, true>;
+        else
+            kern = use_tma ? k_temporal<T, CY, R, S, true, true, 1> : k_temporal<T, CY, R, S, false, true, 1>;
     } else if constexpr (PS) {
         kern = use_tma ? k_temporal<T, CY, R, S, true, false, 1, false, false, false, false, true>
                        : k_temporal<T, CY, R, S, false, false, 1>;
@@ -1553,7 +1668,14 @@ static int launch_cfg(const LaunchReq &q) {
     CompLayout L;
     if (comp) {
         comp_layout<T, CY>(q.nx, q.ny, q.zhi - q.zlo, q.off, aligned, &L);
-        const int64_t need = 8 * (L.nx_stash + L.ny_stash + L.nz_stash);
+        if constexpr (DYN) {
+            // whole columns: no z chunks, no z band
+            L.zc = q.zhi - q.zlo;
+            L.nchunks = 1;
+            L.nz_stash = 0;
+        }
+        const int64_t dyn_extra = DYN ? (int64_t)p.ntiles * 4 + 2 * (q.zhi - q.zlo) * p.ntiles + 64 : 0;
+        const int64_t need = 8 * (L.nx_stash + L.ny_stash + L.nz_stash) + dyn_extra;
         if (need > q.ws_bytes)
             return set_error(SP_EINVAL, "compressed pass needs %lld workspace bytes, got %lld",
                              (long long)need, (long long)q.ws_bytes);
@@ -1565,6 +1687,13 @@ static int launch_cfg(const LaunchReq &q) {
         p.stash_z = p.stash_y + L.ny_stash;
         p.wx2 = L.wx2;
         p.hy2 = L.hy2;
+        if constexpr (DYN) {
+            char *e = reinterpret_cast<char *>(p.stash_z + L.nz_stash);
+            p.progress = reinterpret_cast<int *>(e);
+            p.flag_y = reinterpret_cast<unsigned char *>(e + (int64_t)p.ntiles * 4);
+            p.flag_x = p.flag_y + (q.zhi - q.zlo) * p.ntiles;
+            cudaMemsetAsync(e, 0, (size_t)((int64_t)p.ntiles * 4 + 2 * (q.zhi - q.zlo) * p.ntiles), q.stream);
+        }
     } else {
         // z-chunking: choose the chunk count minimising (waves x steps per chunk)
         int64_t zc = tuning().zchunk;
@@ -1690,6 +1819,9 @@ static int launch_cfg(const LaunchReq &q) {
     u.wx2 = p.wx2;
     u.hy2 = p.hy2;
     u.sxpad = p.ex0 & 1;
+    u.flag_y = DYN ? p.flag_y : nullptr;
+    u.flag_x = DYN ? p.flag_x : nullptr;
+    u.ntiles = p.ntiles;
     const int64_t depth_ = q.zhi - q.zlo;
     if (L.hy2 > 0) {
         k_unstash_y<<<(unsigned)(depth_ * L.hy2), 128, 0, q.stream>>>(u);
@@ -1958,6 +2090,9 @@ static int dispatch(int levels, const LaunchReq &q) {
 #endif
     if (q.mirror) return dispatch_mirror(levels, q);
     if (q.direction != 0) {
+#if SP200_AB
+        if (levels == 4 && tuning().k3_dyn) return launch_cfg<4, 32, 4, 4, 1, false, false, false, false, true>(q);
+#endif
         // K3: the CY = 32 instances, the geometry compressed_workspace sizes
         switch (levels) {
         case 1: return launch_cfg<1, 32, 4, 4>(q);
@@ -2067,7 +2202,16 @@ static int64_t comp_bytes_max(int64_t nx, int64_t ny, int64_t depth) {
         comp_layout<T, 32>(nx, ny, depth, (T - 1) + par, true, &L);
         best = std::max(best, L.nx_stash + L.ny_stash + L.nz_stash);
     }
-    return 8 * best + 256;
+    int64_t extra = 0;
+#if SP200_AB
+    {
+        // the DYN variant's progress counters and stash flags (A/B builds)
+        int ox, ex0, tx, ty;
+        tile_geometry<T, 32>(nx, ny, 0, false, &ox, &ex0, &tx, &ty);
+        extra = (int64_t)tx * ty * (4 + 2 * depth) + 64;
+    }
+#endif
+    return 8 * best + 256 + extra;
 }
 
 int64_t compressed_workspace(int64_t nx, int64_t ny, int64_t depth, int levels) {
