@@ -263,7 +263,10 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
         const int tcount = second ? p.tile_count2 : p.tile_count, uzc = second ? p.zc2 : p.zc;
         tile = (second ? p.tile_base2 : p.tile_base) + ucid % tcount;
         chunk = ucid / tcount;
-        if constexpr (DYN) tile = dyn_tile_of(ucid, p.tiles_x, p.tiles_y, p.direction > 0);
+        if constexpr (DYN) {
+            // p.debug bit 32 (A/B): keep the tile-fastest order
+            if (!(p.debug & 32)) tile = dyn_tile_of(ucid, p.tiles_x, p.tiles_y, p.direction > 0);
+        }
         z0 = p.zlo + chunk * uzc;
         z1 = min(z0 + uzc, p.zhi);
     } else {
@@ -366,6 +369,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     // DYN: the tiles that read this tile's bands (forward: lower neighbours)
     [[maybe_unused]] int rd_y = -1, rd_x = -1, rd_d = -1;
     [[maybe_unused]] int c_y = 0x7fffffff, c_x = 0x7fffffff, c_d = 0x7fffffff;  // cached progress
+    [[maybe_unused]] int l_y = 0, l_x = 0, l_d = 0;                                // loads in flight
     [[maybe_unused]] double *icol = dcol + (int64_t)p.doff * pz;                // in-place column
     if constexpr (DYN) {
         const int dy = fwd ? -1 : 1, dx = fwd ? -1 : 1;
@@ -658,13 +662,22 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
                 // reading them must have loaded (forward: the lower x, y and
                 // diagonal neighbours; a y-band row also covers the corner
                 // columns the x neighbour reads)
+                // counters loaded one step earlier (relaxed, never waited on
+                // in the step that issues them); the decision depends on the
+                // loaded values, so no band store can precede its load
+                c_y = max(c_y, l_y);
+                c_x = max(c_x, l_x);
+                c_d = max(c_d, l_d);
                 const int pn = z0 - T + (s + 1) - 2 * T + 1;
                 const int need = (fwd ? pn - T : pn + T) + 1;
-                if (c_y < need) c_y = ld_acquire_s32(p.progress + rd_y);
-                if (c_x < need) c_x = ld_acquire_s32(p.progress + rd_x);
-                if (c_d < need) c_d = ld_acquire_s32(p.progress + rd_d);
-                const bool xi = c_x >= need, yi = xi && c_y >= need && c_d >= need;
+                // p.debug bit 16 (A/B): stash every band (the DYN schedule alone)
+                const bool xi = c_x >= need && !(p.debug & 16), yi = xi && c_y >= need && c_d >= need;
                 reinterpret_cast<volatile int *>(bar + C::NBAR)[(s + 1) & 1] = (yi ? 1 : 0) | (xi ? 2 : 0);
+                // prefetch for the next step's decision when the cached value
+                // may not cover it
+                if (c_y < need + 2) l_y = ld_relaxed_s32(p.progress + rd_y);
+                if (c_x < need + 2) l_x = ld_relaxed_s32(p.progress + rd_x);
+                if (c_d < need + 2) l_d = ld_relaxed_s32(p.progress + rd_d);
             }
         }
         const double *cur = stage + si * PLANE_AL;
