@@ -318,7 +318,7 @@ int sp_set_tuning(int key, int64_t value) {
     case 8: t.zchunk2 = value; return SP_OK;
     case 10: t.k3_dyn = value; return SP_OK;
     case 9:
-        if (value < 0 || value > 5) return set_error(SP_EINVAL, "k2 layout %lld outside [0, 5]", (long long)value);
+        if (value < 0 || value > 15) return set_error(SP_EINVAL, "k2 layout %lld outside [0, 15]", (long long)value);
         t.k2_layout = value;
         return SP_OK;
     case 2: {

@@ -43,6 +43,9 @@
 
 namespace sp200 {
 
+// K3 in place: one progress counter per 128-byte line
+constexpr int PROG_STRIDE = 32;
+
 struct TParams {
     const double *src;
     double *dst;
@@ -67,29 +70,13 @@ struct TParams {
     int wx2, hy2;    // stash_x row width, stash_y rows per plane
     int debug;       // profiling only (sp_set_tuning key 4): 1 skip levels, 2 skip loads, 4 skip barrier
     int c0;          // k_col: stage column of region column 0 (2 or 3: even TMA box start)
-    // K3 DYN (A/B): band outputs go in place when the neighbour that reads
-    // them has already loaded that plane (its progress counter), else to
-    // the stash, flagged per (plane, tile) for the unstash kernels
-    int *progress;            // [ntiles] input planes fully loaded (+1), per launch
-    unsigned char *flag_y, *flag_x;  // [depth][ntiles]: band stashed at this output plane
+    // K3 in place (DYN): every output is stored in place; a tile's stores of
+    // a plane wait until the tiles that read the cells they overwrite have
+    // loaded that plane (per-tile progress counters, tiles taken in
+    // dependency order through a ticket)
+    int *progress;            // [ntiles] input planes loaded (count), then [ntiles] = the ticket
+    unsigned char *flag_y, *flag_x;  // unstash: null = copy all (kept for the kernels' ABI)
 };
-
-// DYN launch order: tiles by anti-diagonal tx + ty, ascending for forward
-// passes (the lower neighbours that read a tile's bands start first),
-// descending for backward passes
-__device__ __forceinline__ int dyn_tile_of(int c, int tiles_x, int tiles_y, bool fwd) {
-    const int n = tiles_x * tiles_y;
-    if (!fwd) c = n - 1 - c;
-    for (int d = 0;; ++d) {
-        const int lo = max(0, d - (tiles_y - 1)), hi = min(d, tiles_x - 1);
-        const int cnt = hi - lo + 1;
-        if (c < cnt) {
-            const int tx = lo + c;
-            return (d - tx) * tiles_x + tx;
-        }
-        c -= cnt;
-    }
-}
 
 template <int T, int CY, int R, int S>
 struct KCfg {
@@ -220,8 +207,9 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
                 for (int si = 0; si < S; ++si) mbar_init(&bar[C::NBAR + si], NW);
             }
             if constexpr (DYN) {
-                reinterpret_cast<int *>(bar + C::NBAR)[0] = 0;  // stash everything until decided
-                reinterpret_cast<int *>(bar + C::NBAR)[1] = 0;
+                // tiles are taken in dependency order: a CTA only ever waits
+                // for tiles with a lower ticket, which are running or done
+                reinterpret_cast<int *>(bar + C::NBAR)[0] = atomicAdd(p.progress + (int64_t)p.ntiles * PROG_STRIDE, 1);
             }
             if constexpr (CL > 1) {
                 // arm phase 0 of every halo barrier: 64 doubles per row
@@ -264,8 +252,11 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
         tile = (second ? p.tile_base2 : p.tile_base) + ucid % tcount;
         chunk = ucid / tcount;
         if constexpr (DYN) {
-            // p.debug bit 32 (A/B): keep the tile-fastest order
-            if (!(p.debug & 32)) tile = dyn_tile_of(ucid, p.tiles_x, p.tiles_y, p.direction > 0);
+            // forward passes overwrite cells the lower neighbours read, so
+            // tiles run in ascending order; backward passes in descending
+            const int tk = reinterpret_cast<volatile int *>(bar + C::NBAR)[0];
+            tile = p.direction > 0 ? tk : p.ntiles - 1 - tk;
+            chunk = 0;
         }
         z0 = p.zlo + chunk * uzc;
         z1 = min(z0 + uzc, p.zhi);
@@ -336,8 +327,8 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     const bool fwd = p.direction > 0;
     const int sxpad = p.ex0 & 1;
     const int xo0 = rx0 + i0 - x0;  // stored-tile column of the lane's first cell
-    const bool xband = COMP && (fwd ? (tx > 0 && xo0 < 2 * T)
-                                    : (tx < p.tiles_x - 1 && xo0 >= p.ox - 2 * T - sxpad));
+    const bool xband = COMP && !DYN && (fwd ? (tx > 0 && xo0 < 2 * T)
+                                            : (tx < p.tiles_x - 1 && xo0 >= p.ox - 2 * T - sxpad));
     bool yb[R];
     int ky0;
     {
@@ -347,10 +338,10 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int yo = ry0 + j0 + r - y0;
-        yb[r] = COMP && (fwd ? (ty > 0 && yo < 2 * T) : (ty < p.tiles_y - 1 && yo >= OYc - 2 * T));
+        yb[r] = COMP && !DYN && (fwd ? (ty > 0 && yo < 2 * T) : (ty < p.tiles_y - 1 && yo >= OYc - 2 * T));
     }
     const int nchunks = (p.zhi - p.zlo + p.zc - 1) / p.zc;
-    const bool zband_chunk = COMP && (fwd ? chunk > 0 : chunk < nchunks - 1);
+    const bool zband_chunk = COMP && !DYN && (fwd ? chunk > 0 : chunk < nchunks - 1);
     // destinations, affine in the output plane pout and the row r:
     //   in place / x stash: ncol + pout * npz + r * nrs
     //   y stash: sy_col + (pout * hy2 + r) * srow;  z stash: sz_col + (kz * ny + r) * srow
@@ -366,17 +357,21 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
         nrs = p.wx2;
     }
     const bool npair = x_out[0] && x_out[1] && (xband || p.pair_store);
-    // DYN: the tiles that read this tile's bands (forward: lower neighbours)
+    // DYN: the tiles that read the cells this tile's shifted stores overwrite
+    // (forward: the lower x, y and diagonal neighbours), their cached
+    // progress and the relaxed loads in flight
     [[maybe_unused]] int rd_y = -1, rd_x = -1, rd_d = -1;
-    [[maybe_unused]] int c_y = 0x7fffffff, c_x = 0x7fffffff, c_d = 0x7fffffff;  // cached progress
-    [[maybe_unused]] int l_y = 0, l_x = 0, l_d = 0;                                // loads in flight
-    [[maybe_unused]] double *icol = dcol + (int64_t)p.doff * pz;                // in-place column
+    [[maybe_unused]] int l_y = 0x7fffffff, l_x = 0x7fffffff, l_d = 0x7fffffff;
+    [[maybe_unused]] int q_y[2] = {0, 0}, q_x[2] = {0, 0}, q_d[2] = {0, 0};  // polls in flight, by step parity
     if constexpr (DYN) {
-        const int dy = fwd ? -1 : 1, dx = fwd ? -1 : 1;
+        const int dd = fwd ? -1 : 1;
         const bool hy = fwd ? ty > 0 : ty < p.tiles_y - 1, hx = fwd ? tx > 0 : tx < p.tiles_x - 1;
-        if (hy) { rd_y = tile + dy * p.tiles_x; c_y = -0x7fffffff; }
-        if (hx) { rd_x = tile + dx; c_x = -0x7fffffff; }
-        if (hx && hy) { rd_d = tile + dy * p.tiles_x + dx; c_d = -0x7fffffff; }
+        if (hy) rd_y = tile + dd * p.tiles_x;
+        if (hx) rd_x = tile + dd;
+        if (hx && hy) rd_d = tile + dd * p.tiles_x + dd;
+        l_y = hy ? 0 : 0x7fffffff;
+        l_x = hx ? 0 : 0x7fffffff;
+        l_d = (hx && hy) ? 0 : 0x7fffffff;
     }
     double *sy_col = COMP ? p.stash_y + ((int64_t)ky0 - (int64_t)p.zlo * p.hy2) * srow + rx0 + i0 + sxpad
                           : nullptr;
@@ -456,17 +451,10 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
             const bool store_plane = (u == T) && pout >= z0 && pout < z1;
             // K3 destinations of this level-T plane
             [[maybe_unused]] double *nrow = nullptr, *yrow = nullptr, *zrow = nullptr;
-            [[maybe_unused]] bool zb = false, dyn_yin = false, dyn_xin = false;
+            [[maybe_unused]] bool zb = false;
             if constexpr (COMP) {
                 if (u == T) {
                     nrow = ncol + (int64_t)pout * npz;
-                    if constexpr (DYN) {
-                        // the CTA-wide decision for this plane (thread 0, one
-                        // step earlier, published by the step barrier)
-                        const int w = reinterpret_cast<volatile int *>(bar + C::NBAR)[s & 1];
-                        dyn_yin = (w & 1) != 0;
-                        dyn_xin = (w & 2) != 0;
-                    }
                     const int zo = pout - z0;
                     zb = zband_chunk && (unsigned)(zo - zb_lo) < (unsigned)(2 * T);
                     zrow = sz_col + (int64_t)(zo + kz_off) * zstride;
@@ -570,10 +558,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
                         // in the same order); y and z bands are whole rows
                         double *row = nrow + (int64_t)r * nrs;
                         bool pr = npair;
-                        if (DYN && ((yb[r] && dyn_yin) || (!yb[r] && xband && dyn_xin))) {
-                            row = icol + (int64_t)pout * pz + (int64_t)r * p.ex;
-                            pr = x_out[0] && x_out[1] && p.pair_store;
-                        } else if (yb[r]) {
+                        if (yb[r]) {
                             row = yrow + (int64_t)r * srow;
                             pr = x_out[0] && x_out[1];
                         } else if (zb) {
@@ -600,21 +585,6 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
                             }
                         }
                     }
-                }
-            }
-            if constexpr (DYN) {
-                // flag the bands of this plane that went to the stash
-                if (u == T && store_plane && lane == 0) {
-                    bool any_y = false, any_n = false;
-#pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        if (!y_out[r]) continue;
-                        if (yb[r]) any_y = true;
-                        else any_n = true;
-                    }
-                    const int64_t fi = (int64_t)(pout - p.zlo) * p.ntiles + tile;
-                    if (any_y && !dyn_yin) p.flag_y[fi] = 1;
-                    if (any_n && rd_x >= 0 && !dyn_xin) p.flag_x[fi] = 1;
                 }
             }
         }
@@ -644,6 +614,46 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
                 issue(t);
             }
         } else {
+        if constexpr (DYN) {
+            // polled by the last warp: it covers ghost rows above the stored
+            // tile and has fewer stores per step than the interior warps, so
+            // the few dozen instructions here do not make it the last one at
+            // the barrier
+            if (tid == NT - 32) {
+                // this step's level-T stores (plane index s - 2T + 1 of the
+                // column) land on input plane s - 2T + 1 -/+ T of the source
+                // frame: the neighbours must have loaded it.  l_* were loaded
+                // one step ago (never waited on in the step that issues them).
+                const int need = s - 2 * T + 1 + (fwd ? -T : T) + 1;
+                // polls issued two steps ago (a counter line that another SM
+                // keeps writing takes longer than one step to read)
+                constexpr int QQ = decltype(Qc)::value;
+                l_y = max(l_y, q_y[QQ]);
+                l_x = max(l_x, q_x[QQ]);
+                l_d = max(l_d, q_d[QQ]);
+                if (min(l_y, min(l_x, l_d)) < need) {
+                    int spins = 0;
+                    for (;;) {
+                        int c = 0x7fffffff;
+                        if (rd_y >= 0) c = min(c, ld_acquire_s32(p.progress + rd_y * PROG_STRIDE));
+                        if (rd_x >= 0) c = min(c, ld_acquire_s32(p.progress + rd_x * PROG_STRIDE));
+                        if (rd_d >= 0) c = min(c, ld_acquire_s32(p.progress + rd_d * PROG_STRIDE));
+                        if (c >= need) break;
+                        if (++spins > (1 << 26)) __trap();  // a broken dependency order, never a slow neighbour
+                        __nanosleep(32);
+                    }
+                }
+                // re-poll a neighbour only when its last seen count runs out
+                // within three steps (forward passes have 3T-1 planes of
+                // slack, so this is one poll every ~10 steps; backward T-1)
+                {
+                    const int soon = need + 3;
+                    if (rd_y >= 0 && l_y < soon) q_y[QQ] = ld_relaxed_s32(p.progress + rd_y * PROG_STRIDE);
+                    if (rd_x >= 0 && l_x < soon) q_x[QQ] = ld_relaxed_s32(p.progress + rd_x * PROG_STRIDE);
+                    if (rd_d >= 0 && l_d < soon) q_d[QQ] = ld_relaxed_s32(p.progress + rd_d * PROG_STRIDE);
+                }
+            }
+        }
         if (!(SP200_PROFILE_KNOBS && (p.debug & 4))) __syncthreads();
         if constexpr (TMA) {
             if (tid == 0 && s + PD < nload && !(SP200_PROFILE_KNOBS && (p.debug & 2))) issue(s + PD);
@@ -653,31 +663,25 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
         }
         }
         if constexpr (DYN) {
+            // published by thread 0 after the barrier (warp 0 covers ghost
+            // rows too); every counter has its own 128-byte line: counters
+            // sharing a sector ran 3x slower
             if (tid == 0) {
-                // every thread has waited for the stage of input plane z0-T+s:
-                // this tile no longer reads that plane from global memory
-                if (s < nload) st_relaxed_s32(p.progress + tile, z0 - T + s + 1);
-                // decide for the plane level T emits at step s+1: its band
-                // outputs overwrite input plane pout -/+ T, which every tile
-                // reading them must have loaded (forward: the lower x, y and
-                // diagonal neighbours; a y-band row also covers the corner
-                // columns the x neighbour reads)
-                // counters loaded one step earlier (relaxed, never waited on
-                // in the step that issues them); the decision depends on the
-                // loaded values, so no band store can precede its load
-                c_y = max(c_y, l_y);
-                c_x = max(c_x, l_x);
-                c_d = max(c_d, l_d);
-                const int pn = z0 - T + (s + 1) - 2 * T + 1;
-                const int need = (fwd ? pn - T : pn + T) + 1;
-                // p.debug bit 16 (A/B): stash every band (the DYN schedule alone)
-                const bool xi = c_x >= need && !(p.debug & 16), yi = xi && c_y >= need && c_d >= need;
-                reinterpret_cast<volatile int *>(bar + C::NBAR)[(s + 1) & 1] = (yi ? 1 : 0) | (xi ? 2 : 0);
-                // prefetch for the next step's decision when the cached value
-                // may not cover it
-                if (c_y < need + 2) l_y = ld_relaxed_s32(p.progress + rd_y);
-                if (c_x < need + 2) l_x = ld_relaxed_s32(p.progress + rd_x);
-                if (c_d < need + 2) l_d = ld_relaxed_s32(p.progress + rd_d);
+                // input planes this tile has in shared memory: step s's, plus
+                // the prefetched stages that have already landed
+                if (s < nload) {
+                    int done = s + 1;
+                    if constexpr (TMA) {
+#pragma unroll
+                        for (int a = 1; a < PD; ++a) {
+                            const uint32_t g = gbase + (uint32_t)(s + a);
+                            if (done == s + a && s + a < nload && mbar_test_wait(&bar[g % S], (g / S) & 1u)) done = s + a + 1;
+                        }
+                    }
+                    st_relaxed_s32(p.progress + tile * PROG_STRIDE, done);
+                } else if (s == nload) {
+                    st_relaxed_s32(p.progress + tile * PROG_STRIDE, 0x7ffffff0);
+                }
             }
         }
         const double *cur = stage + si * PLANE_AL;
@@ -750,6 +754,10 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     // no CTA leaves while a peer may still address its shared memory
     if constexpr (CL > 1) cluster_sync_all();
 }
+
+}  // namespace sp200
+#include "sp200_tmem.cuh"
+namespace sp200 {
 
 
 #if SP200_AB
@@ -1682,12 +1690,14 @@ static int launch_cfg(const LaunchReq &q) {
     if (comp) {
         comp_layout<T, CY>(q.nx, q.ny, q.zhi - q.zlo, q.off, aligned, &L);
         if constexpr (DYN) {
-            // whole columns: no z chunks, no z band
+            // whole columns, everything in place: no stash, one progress
+            // counter per tile and the ticket
             L.zc = q.zhi - q.zlo;
             L.nchunks = 1;
-            L.nz_stash = 0;
+            L.nx_stash = L.ny_stash = L.nz_stash = 0;
+            L.wx2 = L.hy2 = 0;
         }
-        const int64_t dyn_extra = DYN ? (int64_t)p.ntiles * 4 + 2 * (q.zhi - q.zlo) * p.ntiles + 64 : 0;
+        const int64_t dyn_extra = DYN ? ((int64_t)p.ntiles + 1) * 4 * PROG_STRIDE : 0;
         const int64_t need = 8 * (L.nx_stash + L.ny_stash + L.nz_stash) + dyn_extra;
         if (need > q.ws_bytes)
             return set_error(SP_EINVAL, "compressed pass needs %lld workspace bytes, got %lld",
@@ -1701,11 +1711,8 @@ static int launch_cfg(const LaunchReq &q) {
         p.wx2 = L.wx2;
         p.hy2 = L.hy2;
         if constexpr (DYN) {
-            char *e = reinterpret_cast<char *>(p.stash_z + L.nz_stash);
-            p.progress = reinterpret_cast<int *>(e);
-            p.flag_y = reinterpret_cast<unsigned char *>(e + (int64_t)p.ntiles * 4);
-            p.flag_x = p.flag_y + (q.zhi - q.zlo) * p.ntiles;
-            cudaMemsetAsync(e, 0, (size_t)((int64_t)p.ntiles * 4 + 2 * (q.zhi - q.zlo) * p.ntiles), q.stream);
+            p.progress = reinterpret_cast<int *>(ws);
+            cudaMemsetAsync(ws, 0, (size_t)dyn_extra, q.stream);
         }
     } else {
         // z-chunking: choose the chunk count minimising (waves x steps per chunk)
@@ -1808,7 +1815,7 @@ static int launch_cfg(const LaunchReq &q) {
     launch_units<CL>(kern, grid, C::NT, SMEM_B, q.stream, p, tmap);
     count_launch();
     int rc = check_launch("k_temporal");
-    if (rc || !comp) return rc;
+    if (rc || !comp || DYN) return rc;
     UnstashArgs u;
     u.data = q.dst;
     u.ex = q.ex;
@@ -1832,8 +1839,8 @@ static int launch_cfg(const LaunchReq &q) {
     u.wx2 = p.wx2;
     u.hy2 = p.hy2;
     u.sxpad = p.ex0 & 1;
-    u.flag_y = DYN ? p.flag_y : nullptr;
-    u.flag_x = DYN ? p.flag_x : nullptr;
+    u.flag_y = nullptr;
+    u.flag_x = nullptr;
     u.ntiles = p.ntiles;
     const int64_t depth_ = q.zhi - q.zlo;
     if (L.hy2 > 0) {
@@ -1853,6 +1860,88 @@ static int launch_cfg(const LaunchReq &q) {
     return rc;
 }
 
+
+
+// Host launch of k_tm (two-grid fused passes, TMA loader, pair-aligned
+// frames): launch_cfg's geometry and split schedule with the 64 x NW*R region.
+template <int T, int R, int NW, int S, int NSPT>
+static int launch_tm(const LaunchReq &q) {
+    using C = TMCfg<T, R, NW, S, NSPT>;
+    constexpr int CY = C::CY;
+    TParams p;
+    memset(&p, 0, sizeof(p));
+    int tiles_y;
+    tile_geometry<T, CY>(q.nx, q.ny, q.off, true, &p.ox, &p.ex0, &p.tiles_x, &tiles_y);
+    p.src = q.src;
+    p.dst = q.dst;
+    p.ex = q.ex;
+    p.ey = q.ey;
+    p.ez = q.ez;
+    p.nx = (int)q.nx;
+    p.ny = (int)q.ny;
+    p.nz = (int)q.nz;
+    p.off = (int)q.off;
+    p.doff = (int)q.doff;
+    p.pair_store = ((q.off - q.doff) % 2 == 0) ? 1 : 0;
+    p.tiles_y = tiles_y;
+    p.ntiles = p.tiles_x * tiles_y;
+    p.zlo = (int)q.zlo;
+    p.zhi = (int)q.zhi;
+    void (*kern)(const TParams, const CUtensorMap);
+    if (q.mirror) {
+        p.mir = q.mirror + q.mirror_zshift * q.ex * q.ey;
+        kern = k_tm<T, R, NW, S, NSPT, true>;
+    } else {
+        kern = k_tm<T, R, NW, S, NSPT, false>;
+    }
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return set_error(SP_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    const int64_t slots = sm_count();
+    const int64_t depth = q.zhi - q.zlo;
+    CUtensorMap tmap;
+    memset(&tmap, 0, sizeof(tmap));
+    {
+        cuuint64_t dims[3] = {(cuuint64_t)q.ex, (cuuint64_t)q.ey, (cuuint64_t)q.ez};
+        cuuint64_t strides[2] = {(cuuint64_t)(q.ex * 8), (cuuint64_t)(q.ex * q.ey * 8)};
+        cuuint32_t box[3] = {(cuuint32_t)C::SPX, (cuuint32_t)C::PY, 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        CUresult r = encode_fn()(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)q.src, dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return set_error(SP_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    }
+    p.tile_base = 0;
+    p.tile_count = p.ntiles;
+    p.split = 0x7fffffff;
+    int64_t grid;
+    if (tuning().zchunk <= 0 && p.ntiles >= slots) {
+        // one grid: `full` tiles march their whole column, the rest follow in
+        // blockIdx order as z-chunks sized to fill one more wave
+        const int full = (int)((p.ntiles / slots) * slots);
+        const int rem = p.ntiles - full;
+        p.tile_count = full;
+        p.zc = (int)depth;
+        grid = full;
+        if (rem > 0) {
+            p.split = full;
+            p.tile_base2 = full;
+            p.tile_count2 = rem;
+            const int64_t zcb = tuning().zchunk2 > 0 ? std::min<int64_t>(tuning().zchunk2, depth)
+                                                     : pick_zchunk(depth, rem, slots, T);
+            p.zc2 = (int)zcb;
+            grid += (int64_t)rem * ((depth + zcb - 1) / zcb);
+        }
+    } else {
+        int64_t zc = tuning().zchunk > 0 ? tuning().zchunk : pick_zchunk(depth, p.ntiles, slots, T);
+        if (zc < 1) zc = 1;
+        p.zc = (int)zc;
+        grid = (int64_t)p.ntiles * ((depth + zc - 1) / zc);
+    }
+    if (grid > 0x7fffffff) return set_error(SP_EUNSUP, "grid too large");
+    kern<<<(unsigned)grid, C::NT, C::SMEM, q.stream>>>(p, tmap);
+    count_launch();
+    return check_launch("k_tm");
+}
 
 #if SP200_AB
 
@@ -2101,11 +2190,19 @@ static int dispatch(int levels, const LaunchReq &q) {
         return q.mirror ? dispatch_col<true>(levels, q, xs) : dispatch_col<false>(levels, q, xs);
     }
 #endif
+    if (q.direction == 0 && levels == 4 && !q.ring && tuning().k2_layout >= 6 && uses_tma(q)) {
+        if (tuning().k2_layout == 6) return launch_tm<4, 4, 12, 4, 2>(q);
+        if (tuning().k2_layout == 7) return launch_tm<4, 6, 8, 4, 2>(q);
+        if (tuning().k2_layout == 8) return launch_tm<4, 4, 8, 4, 0>(q);
+        if (tuning().k2_layout == 9) return launch_tm<4, 4, 8, 4, 2>(q);
+        if (tuning().k2_layout == 10) return launch_tm<4, 4, 8, 4, 4>(q);
+    }
     if (q.mirror) return dispatch_mirror(levels, q);
     if (q.direction != 0) {
-#if SP200_AB
-        if (levels == 4 && tuning().k3_dyn) return launch_cfg<4, 32, 4, 4, 1, false, false, false, false, true>(q);
-#endif
+        // T = 4 (the default depth): everything stored in place, ordered by
+        // per-tile progress counters; tuning key 10 = 1 keeps the band stash
+        if (levels == 4 && !tuning().k3_dyn && uses_tma(q))
+            return launch_cfg<4, 32, 4, 4, 1, false, false, false, false, true>(q);
         // K3: the CY = 32 instances, the geometry compressed_workspace sizes
         switch (levels) {
         case 1: return launch_cfg<1, 32, 4, 4>(q);
@@ -2215,15 +2312,10 @@ static int64_t comp_bytes_max(int64_t nx, int64_t ny, int64_t depth) {
         comp_layout<T, 32>(nx, ny, depth, (T - 1) + par, true, &L);
         best = std::max(best, L.nx_stash + L.ny_stash + L.nz_stash);
     }
-    int64_t extra = 0;
-#if SP200_AB
-    {
-        // the DYN variant's progress counters and stash flags (A/B builds)
-        int ox, ex0, tx, ty;
-        tile_geometry<T, 32>(nx, ny, 0, false, &ox, &ex0, &tx, &ty);
-        extra = (int64_t)tx * ty * (4 + 2 * depth) + 64;
-    }
-#endif
+    // the in-place pass's progress counters and ticket
+    int ox, ex0, tx, ty;
+    tile_geometry<T, 32>(nx, ny, 0, false, &ox, &ex0, &tx, &ty);
+    const int64_t extra = ((int64_t)tx * ty + 1) * 4 * PROG_STRIDE + 64;
     return 8 * best + 256 + extra;
 }
 
