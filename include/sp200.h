@@ -144,15 +144,24 @@ int sp_temporal(const double *src, double *dst, int64_t ex, int64_t ey, int64_t 
  * fused into one HBM pass frame a0 -> a0 + s*levels.  `src_off` = pad + 1 - a0.
  * Ring cells are read at the source frame (the caller writes the faces there
  * first); the faces are written at the destination frame afterwards when
- * faces != NULL.  Outputs whose shifted store would land in another tile's
- * read region go through `workspace` (a band stash) and are copied into place
- * by a second kernel, so no inter-CTA ordering is needed.
+ * faces != NULL.  A tile's shifted stores land in the read regions of its
+ * lower (forward) or upper (backward) neighbours.  At levels = 4 on a
+ * TMA-eligible array every output is stored in place: tiles are taken in
+ * dependency order and a tile's stores of a plane wait until those neighbours
+ * have loaded it (per-tile progress counters in `workspace`, 128 bytes per
+ * tile).  Otherwise the outputs that would land in another tile's read
+ * region go through `workspace` (a band stash) and are copied into place by
+ * a second kernel.
  * sp_compressed_workspace() returns the workspace bytes for a pass over
- * `depth` = zhi - zlo planes (the worst case over the tile layouts a launch
- * may pick); sp_compressed returns SP_EINVAL when `workspace_bytes` is
- * smaller than the layout of this launch needs.
+ * `depth` = zhi - zlo planes, the worst case over every path and tile layout
+ * a launch may pick; sp_compressed_workspace_for() returns the bytes for the
+ * path sp_compressed takes on this array (the in-place pass needs no stash).
+ * sp_compressed returns SP_EINVAL when `workspace_bytes` is smaller than the
+ * launch needs.
  */
 int64_t sp_compressed_workspace(int64_t nx, int64_t ny, int64_t depth, int levels);
+int64_t sp_compressed_workspace_for(const double *data, int64_t ex, int64_t ey, int64_t nx,
+                                    int64_t ny, int64_t depth, int levels);
 int sp_compressed(double *data, int64_t ex, int64_t ey, int64_t ez,
                   int64_t nx, int64_t ny, int64_t nz, int64_t src_off, int direction,
                   int levels, int64_t zlo, int64_t zhi, void *workspace,

@@ -25,7 +25,7 @@ SP_MAX_FUSED = 4
 EXPORTS = (
     "sp_version", "sp_last_error", "sp_launch_count", "sp_fill_seeded",
     "sp_fill_constant", "sp_sweep", "sp_apply_window", "sp_window_gather",
-    "sp_copy_ring", "sp_rings_equal", "sp_write_faces", "sp_temporal", "sp_compressed_workspace",
+    "sp_copy_ring", "sp_rings_equal", "sp_write_faces", "sp_temporal", "sp_compressed_workspace", "sp_compressed_workspace_for",
     "sp_compressed", "sp_set_tuning", "sp_tma_eligible", "sp_temporal_mirror", "sp_ipc_handle",
     "sp_ipc_open", "sp_ipc_close", "sp_signal", "sp_wait", "sp_pack_boxes", "sp_unpack_boxes",
 )
@@ -64,6 +64,7 @@ def _declare(L):
         "sp_write_faces": ([dp, i64, i64, i64, i64, i64, i64, i64, ctypes.POINTER(dp), i32, vp], i32),
         "sp_temporal": ([dp, dp, i64, i64, i64, i64, i64, i64, i64, i32, i64, i64, vp], i32),
         "sp_compressed_workspace": ([i64, i64, i64, i32], i64),
+        "sp_compressed_workspace_for": ([dp, i64, i64, i64, i64, i64, i32], i64),
         "sp_compressed": ([dp, i64, i64, i64, i64, i64, i64, i64, i32, i32, i64, i64, vp, i64,
                            ctypes.POINTER(dp), i32, vp], i32),
         "sp_set_tuning": ([i32, i64], i32),

@@ -569,6 +569,12 @@ int64_t sp_compressed_workspace(int64_t nx, int64_t ny, int64_t depth, int level
     return compressed_workspace(nx, ny, depth, levels);
 }
 
+int64_t sp_compressed_workspace_for(const double *data, int64_t ex, int64_t ey, int64_t nx, int64_t ny,
+                                    int64_t depth, int levels) {
+    if (nx < 1 || ny < 1 || depth < 1 || levels < 1 || levels > SP_MAX_FUSED) return 0;
+    return compressed_workspace_for(data, ex, ey, nx, ny, depth, levels);
+}
+
 int sp_compressed(double *data, int64_t ex, int64_t ey, int64_t ez, int64_t nx, int64_t ny,
                   int64_t nz, int64_t src_off, int direction, int levels, int64_t zlo,
                   int64_t zhi, void *workspace, int64_t workspace_bytes,

@@ -48,6 +48,8 @@ int launch_temporal_mirror(const double *src, double *dst, int64_t ex, int64_t e
                            cudaStream_t stream);
 bool tma_eligible(const void *ptr, int64_t ex, int64_t ey);
 int64_t compressed_workspace(int64_t nx, int64_t ny, int64_t depth, int levels);
+int64_t compressed_workspace_for(const double *data, int64_t ex, int64_t ey, int64_t nx, int64_t ny,
+                                 int64_t depth, int levels);
 int launch_compressed(double *data, int64_t ex, int64_t ey, int64_t ez, int64_t nx, int64_t ny,
                       int64_t nz, int64_t src_off, int direction, int levels, int64_t zlo,
                       int64_t zhi, void *ws, int64_t ws_bytes, cudaStream_t stream);

@@ -2319,6 +2319,22 @@ static int64_t comp_bytes_max(int64_t nx, int64_t ny, int64_t depth) {
     return 8 * best + 256 + extra;
 }
 
+// The workspace of the launch sp_compressed picks for this array: the in-place
+// pass (T = 4, TMA-eligible array) needs only its progress counters.
+int64_t compressed_workspace_for(const double *data, int64_t ex, int64_t ey, int64_t nx, int64_t ny,
+                                 int64_t depth, int levels) {
+    LaunchReq q{data, const_cast<double *>(data), ex, ey, 0, nx, ny, 0, 0, 0, 0, depth, 1, nullptr, 0, nullptr};
+    if (levels == 4 && !tuning().k3_dyn && data && uses_tma(q)) {
+        int ox, ex0, tx, ty, best = 0;
+        for (int par = 0; par < 2; ++par) {
+            tile_geometry<4, 32>(nx, ny, 3 + par, true, &ox, &ex0, &tx, &ty);
+            best = std::max(best, tx * ty);
+        }
+        return ((int64_t)best + 1) * 4 * PROG_STRIDE + 256;
+    }
+    return compressed_workspace(nx, ny, depth, levels);
+}
+
 int64_t compressed_workspace(int64_t nx, int64_t ny, int64_t depth, int levels) {
     switch (levels) {
     case 1: return comp_bytes_max<1>(nx, ny, depth);

@@ -251,7 +251,9 @@ def compressed_pass(grid: Grid3, levels: int, direction: int, src_alignment: int
 
 
 def compressed_workspace(grid: Grid3, levels: int, depth: int | None = None) -> torch.Tensor:
-    """Band-stash workspace for a K3 pass over `depth` planes (default nz)."""
-    n = int(_lib.load().sp_compressed_workspace(grid.nx, grid.ny, grid.nz if depth is None else depth,
-                                                int(levels)))
+    """Workspace for a K3 pass of this grid over `depth` planes (default nz):
+    the progress counters of the in-place pass, or the band stash."""
+    ex, ey, _ = grid.extents
+    n = int(_lib.load().sp_compressed_workspace_for(_ptr(grid.data), ex, ey, grid.nx, grid.ny,
+                                                    grid.nz if depth is None else depth, int(levels)))
     return torch.empty(max(n, 256), dtype=torch.uint8, device=grid.data.device)

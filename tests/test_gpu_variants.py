@@ -65,3 +65,51 @@ def test_split_grid_pass(lib, two_launch, balanced):
     dst = g.copy()
     sp.fused_sweeps(g, dst, 4)
     assert_bitwise(dst.interior_numpy(), exp)
+
+
+@pytest.mark.parametrize("stash", [0, 1])
+@pytest.mark.parametrize("dims,pad", [((700, 500, 40), 4), ((90, 61, 30), 4), ((130, 130, 20), 5),
+                                       ((64, 5, 9), 4)])
+def test_compressed_in_place_and_stash(lib, stash, dims, pad):
+    """K3 at t=4: the default pass stores everything in place (per-tile
+    progress counters, tiles taken in dependency order, two rounds of tiles
+    on the 260-tile shape); tuning key 10 = 1 keeps the band stash and the
+    unstash kernels.  Forward and backward passes, bit-exact against the
+    oracle after every pass."""
+    assert lib.sp_set_tuning(10, stash) == 0
+    try:
+        d0 = oracle.make_storage(*dims, init="random", seed=5, lo=-1.0, hi=1.0)
+        g = sp.create_grid(*dims, pad=pad, init="random", seed=5, lo=-1.0, hi=1.0)
+        cfg = sp.PipelineConfig(spec=sp.BlockSpec(dims[0], 8, 8), t=4, grid_mode="compressed")
+        eng = sp.PipelineEngine(cfg, g)
+        for k in range(1, 4):
+            eng.run_pass()
+            exp = oracle.interior(oracle.sweeps(d0, dims, 4 * k), *dims)
+            assert_bitwise(g.interior_numpy(), exp)
+    finally:
+        lib.sp_set_tuning(10, 0)
+
+
+@pytest.mark.parametrize("layout", [6, 7, 8])
+def test_tmem_state_layouts(lib, layout):
+    """k_tm: K2 at t=4 with the level values parked in tensor memory between
+    steps (tuning key 9 = 6: 12 warps, 64 x 48 region; 7: 8 warps, R = 6;
+    8: the 64 x 32 region), bit-exact on ragged shapes and live z ranges."""
+    assert lib.sp_set_tuning(9, layout) == 0
+    try:
+        for dims in SHAPES + [(700, 500, 24)]:
+            d0 = oracle.make_storage(*dims, init="random", seed=11, ring=0.5)
+            exp = oracle.interior(oracle.sweeps(d0, dims, 4), *dims)
+            g = sp.create_grid(*dims, init="random", seed=11, ring=0.5)
+            dst = g.copy()
+            sp.fused_sweeps(g, dst, 4)
+            assert_bitwise(dst.interior_numpy(), exp)
+            zlo, zhi = 1, dims[2] - 2
+            dst2 = g.copy()
+            dst2.data.fill_(-3.0)
+            sp.fused_sweeps(g, dst2, 4, zlo, zhi)
+            got = dst2.interior_numpy()
+            assert_bitwise(got[zlo:zhi], exp[zlo:zhi])
+            assert np.all(got[:zlo] == -3.0) and np.all(got[zhi:] == -3.0)
+    finally:
+        lib.sp_set_tuning(9, 0)
