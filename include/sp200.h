@@ -232,7 +232,11 @@ int sp_unpack_boxes(double *grid, int64_t ex, int64_t ey, int64_t ez, int nbox,
  *        instead of one grid (A/B only)
  * key 7: split K2 passes as one full column plus an equal piece of the
  *        remaining columns per CTA (A/B only)
- * key 8: z-chunk length of the remaining tiles in a split K2 pass (0 = model) */
+ * key 8: z-chunk length of the remaining tiles in a split K2 pass (0 = model)
+ * key 9: K2 kernel layout (A/B builds only; 0 = the product's lane-pair
+ *        k_temporal, 6-10 = k_tm with the pipeline state in tensor memory)
+ * key 10: 1 = sp_compressed at levels 4 keeps the band stash and the unstash
+ *        kernels instead of storing in place */
 int sp_set_tuning(int key, int64_t value);
 
 /* Query: 1 if the TMA loader applies to a grid with row extent `ex`. */

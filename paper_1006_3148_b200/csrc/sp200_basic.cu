@@ -316,7 +316,7 @@ int sp_set_tuning(int key, int64_t value) {
     case 6: t.two_launch = value; return SP_OK;
     case 7: t.balanced_split = value; return SP_OK;
     case 8: t.zchunk2 = value; return SP_OK;
-    case 10: t.k3_dyn = value; return SP_OK;
+    case 10: t.k3_stash = value; return SP_OK;
     case 9:
         if (value < 0 || value > 15) return set_error(SP_EINVAL, "k2 layout %lld outside [0, 15]", (long long)value);
         t.k2_layout = value;

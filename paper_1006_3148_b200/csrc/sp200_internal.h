@@ -29,7 +29,7 @@ struct Tuning {
     int64_t two_launch = 0;      // K2 split pass as two launches instead of one split grid
     int64_t balanced_split = 0;  // K2 split pass: full column + equal piece per CTA (A/B)
     int64_t zchunk2 = 0;         // K2 split pass: z-chunk length of the remaining tiles (0 = model)
-    int64_t k3_dyn = 0;          // 1: K3 at T=4 keeps the band stash + unstash kernels instead of storing in place (A/B)
+    int64_t k3_stash = 0;          // 1: K3 at T=4 keeps the band stash + unstash kernels instead of storing in place (A/B)
     int64_t k2_layout = 0;       // K2 two-grid kernel: 0 lane pairs, 1 columns, 2 columns + level-1 shuffles
 };
 Tuning &tuning();

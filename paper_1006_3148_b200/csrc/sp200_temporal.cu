@@ -70,12 +70,11 @@ struct TParams {
     int wx2, hy2;    // stash_x row width, stash_y rows per plane
     int debug;       // profiling only (sp_set_tuning key 4): 1 skip levels, 2 skip loads, 4 skip barrier
     int c0;          // k_col: stage column of region column 0 (2 or 3: even TMA box start)
-    // K3 in place (DYN): every output is stored in place; a tile's stores of
+    // K3 in place (INPLACE): every output is stored in place; a tile's stores of
     // a plane wait until the tiles that read the cells they overwrite have
     // loaded that plane (per-tile progress counters, tiles taken in
     // dependency order through a ticket)
     int *progress;            // [ntiles] input planes loaded (count), then [ntiles] = the ticket
-    unsigned char *flag_y, *flag_x;  // unstash: null = copy all (kept for the kernels' ABI)
 };
 
 template <int T, int CY, int R, int S>
@@ -151,7 +150,7 @@ __device__ __forceinline__ void stg2_stream(double *p, double a, double b) {
 // fused in: CTAs whose tile touches a domain face, and every CTA at the two z
 // faces, copy the shell cells of their box from the stage into dst.
 template <int T, int CY, int R, int S, bool TMA, bool COMP, int CL, bool MIR = false, bool WP = false,
-          bool RING = false, bool XS1 = false, bool PS = false, bool DYN = false>
+          bool RING = false, bool XS1 = false, bool PS = false, bool INPLACE = false>
 __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB)
     k_temporal(const TParams p, const __grid_constant__ CUtensorMap tmap) {
     using C = KCfg<T, CY, R, S>;
@@ -164,7 +163,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     // the TMA producer waits on, so a slow warp holds back its neighbours
     // and, S - PD steps later, the producer, but not the whole CTA.
     static_assert(!PS || (TMA && !COMP && CL == 1 && !RING && !WP && S >= 5), "PS: plain TMA two-grid passes");
-    static_assert(!DYN || COMP, "DYN: compressed passes only");
+    static_assert(!INPLACE || COMP, "INPLACE: compressed passes only");
     constexpr int PD = WP ? S - 2 : (PS ? S - 3 : S - 1);  // stage prefetch distance
     constexpr int SPX = C::SPX, C0 = C::C0, PLANE = C::PLANE, PLANE_AL = C::PLANE_AL,
                   NT = C::NT;
@@ -206,7 +205,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
 #pragma unroll
                 for (int si = 0; si < S; ++si) mbar_init(&bar[C::NBAR + si], NW);
             }
-            if constexpr (DYN) {
+            if constexpr (INPLACE) {
                 // tiles are taken in dependency order: a CTA only ever waits
                 // for tiles with a lower ticket, which are running or done
                 reinterpret_cast<int *>(bar + C::NBAR)[0] = atomicAdd(p.progress + (int64_t)p.ntiles * PROG_STRIDE, 1);
@@ -251,7 +250,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
         const int tcount = second ? p.tile_count2 : p.tile_count, uzc = second ? p.zc2 : p.zc;
         tile = (second ? p.tile_base2 : p.tile_base) + ucid % tcount;
         chunk = ucid / tcount;
-        if constexpr (DYN) {
+        if constexpr (INPLACE) {
             // forward passes overwrite cells the lower neighbours read, so
             // tiles run in ascending order; backward passes in descending
             const int tk = reinterpret_cast<volatile int *>(bar + C::NBAR)[0];
@@ -327,7 +326,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     const bool fwd = p.direction > 0;
     const int sxpad = p.ex0 & 1;
     const int xo0 = rx0 + i0 - x0;  // stored-tile column of the lane's first cell
-    const bool xband = COMP && !DYN && (fwd ? (tx > 0 && xo0 < 2 * T)
+    const bool xband = COMP && !INPLACE && (fwd ? (tx > 0 && xo0 < 2 * T)
                                             : (tx < p.tiles_x - 1 && xo0 >= p.ox - 2 * T - sxpad));
     bool yb[R];
     int ky0;
@@ -338,10 +337,10 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int yo = ry0 + j0 + r - y0;
-        yb[r] = COMP && !DYN && (fwd ? (ty > 0 && yo < 2 * T) : (ty < p.tiles_y - 1 && yo >= OYc - 2 * T));
+        yb[r] = COMP && !INPLACE && (fwd ? (ty > 0 && yo < 2 * T) : (ty < p.tiles_y - 1 && yo >= OYc - 2 * T));
     }
     const int nchunks = (p.zhi - p.zlo + p.zc - 1) / p.zc;
-    const bool zband_chunk = COMP && !DYN && (fwd ? chunk > 0 : chunk < nchunks - 1);
+    const bool zband_chunk = COMP && !INPLACE && (fwd ? chunk > 0 : chunk < nchunks - 1);
     // destinations, affine in the output plane pout and the row r:
     //   in place / x stash: ncol + pout * npz + r * nrs
     //   y stash: sy_col + (pout * hy2 + r) * srow;  z stash: sz_col + (kz * ny + r) * srow
@@ -357,13 +356,13 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
         nrs = p.wx2;
     }
     const bool npair = x_out[0] && x_out[1] && (xband || p.pair_store);
-    // DYN: the tiles that read the cells this tile's shifted stores overwrite
+    // INPLACE: the tiles that read the cells this tile's shifted stores overwrite
     // (forward: the lower x, y and diagonal neighbours), their cached
     // progress and the relaxed loads in flight
     [[maybe_unused]] int rd_y = -1, rd_x = -1, rd_d = -1;
     [[maybe_unused]] int l_y = 0x7fffffff, l_x = 0x7fffffff, l_d = 0x7fffffff;
     [[maybe_unused]] int q_y[2] = {0, 0}, q_x[2] = {0, 0}, q_d[2] = {0, 0};  // polls in flight, by step parity
-    if constexpr (DYN) {
+    if constexpr (INPLACE) {
         const int dd = fwd ? -1 : 1;
         const bool hy = fwd ? ty > 0 : ty < p.tiles_y - 1, hx = fwd ? tx > 0 : tx < p.tiles_x - 1;
         if (hy) rd_y = tile + dd * p.tiles_x;
@@ -614,7 +613,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
                 issue(t);
             }
         } else {
-        if constexpr (DYN) {
+        if constexpr (INPLACE) {
             // polled by the last warp: it covers ghost rows above the stored
             // tile and has fewer stores per step than the interior warps, so
             // the few dozen instructions here do not make it the last one at
@@ -662,7 +661,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
             else cp_async_commit();
         }
         }
-        if constexpr (DYN) {
+        if constexpr (INPLACE) {
             // published by thread 0 after the barrier (warp 0 covers ghost
             // rows too); every counter has its own 128-byte line: counters
             // sharing a sector ran 3x slower
@@ -755,9 +754,11 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     if constexpr (CL > 1) cluster_sync_all();
 }
 
+#if SP200_AB
 }  // namespace sp200
 #include "sp200_tmem.cuh"
 namespace sp200 {
+#endif
 
 
 #if SP200_AB
@@ -1304,8 +1305,6 @@ struct UnstashArgs {
     int nx, ny, doff, zlo, zhi, zc, nchunks, ox, oy, tiles_x, tiles_y, T2, fwd, sxpad;
     const double *sx, *sy, *sz;
     int wx2, hy2;
-    const unsigned char *flag_y, *flag_x;  // DYN: per (plane, tile), null = copy all
-    int ntiles;
 };
 
 __device__ __forceinline__ bool band_hit(int v, int tile, int ntiles, int o, int T2, int fwd) {
@@ -1347,14 +1346,6 @@ __global__ void k_unstash_y(UnstashArgs a) {
     if (y >= a.ny) return;
     const double *src = a.sy + (int64_t)blockIdx.x * ((a.nx + 2) & ~1) + a.sxpad;
     double *dst = a.data + ((int64_t)(z + a.doff) * a.ey + (y + a.doff)) * a.ex + a.doff;
-    if (a.flag_y) {
-        // DYN: only the tiles whose band row of this plane went to the stash
-        const int bt = k / a.T2, ty = a.fwd ? bt + 1 : bt;
-        const unsigned char *f = a.flag_y + (int64_t)zr * a.ntiles + (int64_t)ty * a.tiles_x;
-        for (int x = threadIdx.x; x < a.nx; x += blockDim.x)
-            if (f[x / a.ox]) dst[x] = src[x];
-        return;
-    }
     copy_row_batched(dst, src, a.nx);
 }
 
@@ -1420,21 +1411,6 @@ __global__ void __launch_bounds__(64 * UXY) k_unstash_x(UnstashArgs a) {
         const bool pair = ok0 && ok1 && (((drow0 + x) & 1) == 0);
         if (!(ok0 || ok1)) continue;
         unsigned lv = live;
-        if (a.flag_x) {
-            // DYN: rows whose tile kept this plane's x band in place are skipped
-            const int txb = a.fwd ? bt + 1 : bt;
-            int ty2 = y0 / a.oy, yo2 = y0 - ty2 * a.oy;
-#pragma unroll
-            for (int i = 0; i < UB; ++i) {
-                if (!a.flag_x[(int64_t)zr * a.ntiles + (int64_t)ty2 * a.tiles_x + txb]) lv &= ~(1u << i);
-                yo2 += UXY;
-                while (yo2 >= a.oy) {
-                    yo2 -= a.oy;
-                    ++ty2;
-                }
-                if (ty2 >= a.tiles_y) ty2 = a.tiles_y - 1;
-            }
-        }
         double2 v[UB];
 #pragma unroll
         for (int i = 0; i < UB; ++i)
@@ -1579,7 +1555,7 @@ static void comp_layout(int64_t nx, int64_t ny, int64_t depth, int64_t off, bool
 }
 
 template <int T, int CY, int R, int S, int CL = 1, bool MIRROR = false, bool WP = false,
-          bool XS1 = false, bool PS = false, bool DYN = false>
+          bool XS1 = false, bool PS = false, bool INPLACE = false>
 static int launch_cfg(const LaunchReq &q) {
     using C = KCfg<T, CY, R, S>;
     constexpr size_t SMEM_B = C::SMEM + (PS ? 8 * S : 0);  // + the PS empty barriers
@@ -1618,7 +1594,6 @@ static int launch_cfg(const LaunchReq &q) {
     p.zhi = (int)q.zhi;
     p.stash_x = p.stash_y = p.stash_z = nullptr;
     p.progress = nullptr;
-    p.flag_y = p.flag_x = nullptr;
     p.debug = (int)tuning().debug;
     p.wx2 = p.hy2 = 0;
 
@@ -1637,7 +1612,7 @@ static int launch_cfg(const LaunchReq &q) {
         kern = use_tma ? k_temporal<T, CY, R, S, true, false, CL>
                        : k_temporal<T, CY, R, S, false, false, CL>;
     } else if (comp) {
-        if constexpr (DYN)
+        if constexpr (INPLACE)
             kern = use_tma ? k_temporal<T, CY, R, S, true, true, 1, false, false, false, false, false, true>
                            : k_temporal<T, CY, R, S, false, true, 1, false, false, false, false, false, true>;
         else
@@ -1689,7 +1664,7 @@ static int launch_cfg(const LaunchReq &q) {
     CompLayout L;
     if (comp) {
         comp_layout<T, CY>(q.nx, q.ny, q.zhi - q.zlo, q.off, aligned, &L);
-        if constexpr (DYN) {
+        if constexpr (INPLACE) {
             // whole columns, everything in place: no stash, one progress
             // counter per tile and the ticket
             L.zc = q.zhi - q.zlo;
@@ -1697,8 +1672,8 @@ static int launch_cfg(const LaunchReq &q) {
             L.nx_stash = L.ny_stash = L.nz_stash = 0;
             L.wx2 = L.hy2 = 0;
         }
-        const int64_t dyn_extra = DYN ? ((int64_t)p.ntiles + 1) * 4 * PROG_STRIDE : 0;
-        const int64_t need = 8 * (L.nx_stash + L.ny_stash + L.nz_stash) + dyn_extra;
+        const int64_t inplace_bytes = INPLACE ? ((int64_t)p.ntiles + 1) * 4 * PROG_STRIDE : 0;
+        const int64_t need = 8 * (L.nx_stash + L.ny_stash + L.nz_stash) + inplace_bytes;
         if (need > q.ws_bytes)
             return set_error(SP_EINVAL, "compressed pass needs %lld workspace bytes, got %lld",
                              (long long)need, (long long)q.ws_bytes);
@@ -1710,9 +1685,9 @@ static int launch_cfg(const LaunchReq &q) {
         p.stash_z = p.stash_y + L.ny_stash;
         p.wx2 = L.wx2;
         p.hy2 = L.hy2;
-        if constexpr (DYN) {
+        if constexpr (INPLACE) {
             p.progress = reinterpret_cast<int *>(ws);
-            cudaMemsetAsync(ws, 0, (size_t)dyn_extra, q.stream);
+            cudaMemsetAsync(ws, 0, (size_t)inplace_bytes, q.stream);
         }
     } else {
         // z-chunking: choose the chunk count minimising (waves x steps per chunk)
@@ -1815,7 +1790,7 @@ static int launch_cfg(const LaunchReq &q) {
     launch_units<CL>(kern, grid, C::NT, SMEM_B, q.stream, p, tmap);
     count_launch();
     int rc = check_launch("k_temporal");
-    if (rc || !comp || DYN) return rc;
+    if (rc || !comp || INPLACE) return rc;
     UnstashArgs u;
     u.data = q.dst;
     u.ex = q.ex;
@@ -1839,9 +1814,6 @@ static int launch_cfg(const LaunchReq &q) {
     u.wx2 = p.wx2;
     u.hy2 = p.hy2;
     u.sxpad = p.ex0 & 1;
-    u.flag_y = nullptr;
-    u.flag_x = nullptr;
-    u.ntiles = p.ntiles;
     const int64_t depth_ = q.zhi - q.zlo;
     if (L.hy2 > 0) {
         k_unstash_y<<<(unsigned)(depth_ * L.hy2), 128, 0, q.stream>>>(u);
@@ -1861,6 +1833,8 @@ static int launch_cfg(const LaunchReq &q) {
 }
 
 
+
+#if SP200_AB
 
 // Host launch of k_tm (two-grid fused passes, TMA loader, pair-aligned
 // frames): launch_cfg's geometry and split schedule with the 64 x NW*R region.
@@ -1943,7 +1917,6 @@ static int launch_tm(const LaunchReq &q) {
     return check_launch("k_tm");
 }
 
-#if SP200_AB
 
 // Host launch of k_split (A/B: tuning key 9 = 4): the launch_cfg geometry of
 // the T=4 pair layout, 512 threads per CTA.
@@ -2190,6 +2163,8 @@ static int dispatch(int levels, const LaunchReq &q) {
         return q.mirror ? dispatch_col<true>(levels, q, xs) : dispatch_col<false>(levels, q, xs);
     }
 #endif
+#if SP200_AB
+    // k_tm: pipeline state in tensor memory (tuning key 9 = 6..10), DESIGN.md §8
     if (q.direction == 0 && levels == 4 && !q.ring && tuning().k2_layout >= 6 && uses_tma(q)) {
         if (tuning().k2_layout == 6) return launch_tm<4, 4, 12, 4, 2>(q);
         if (tuning().k2_layout == 7) return launch_tm<4, 6, 8, 4, 2>(q);
@@ -2197,11 +2172,12 @@ static int dispatch(int levels, const LaunchReq &q) {
         if (tuning().k2_layout == 9) return launch_tm<4, 4, 8, 4, 2>(q);
         if (tuning().k2_layout == 10) return launch_tm<4, 4, 8, 4, 4>(q);
     }
+#endif
     if (q.mirror) return dispatch_mirror(levels, q);
     if (q.direction != 0) {
         // T = 4 (the default depth): everything stored in place, ordered by
         // per-tile progress counters; tuning key 10 = 1 keeps the band stash
-        if (levels == 4 && !tuning().k3_dyn && uses_tma(q))
+        if (levels == 4 && !tuning().k3_stash && uses_tma(q))
             return launch_cfg<4, 32, 4, 4, 1, false, false, false, false, true>(q);
         // K3: the CY = 32 instances, the geometry compressed_workspace sizes
         switch (levels) {
@@ -2324,7 +2300,7 @@ static int64_t comp_bytes_max(int64_t nx, int64_t ny, int64_t depth) {
 int64_t compressed_workspace_for(const double *data, int64_t ex, int64_t ey, int64_t nx, int64_t ny,
                                  int64_t depth, int levels) {
     LaunchReq q{data, const_cast<double *>(data), ex, ey, 0, nx, ny, 0, 0, 0, 0, depth, 1, nullptr, 0, nullptr};
-    if (levels == 4 && !tuning().k3_dyn && data && uses_tma(q)) {
+    if (levels == 4 && !tuning().k3_stash && data && uses_tma(q)) {
         int ox, ex0, tx, ty, best = 0;
         for (int par = 0; par < 2; ++par) {
             tile_geometry<4, 32>(nx, ny, 3 + par, true, &ox, &ex0, &tx, &ty);
