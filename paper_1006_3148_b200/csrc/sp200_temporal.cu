@@ -613,6 +613,13 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
                 issue(t);
             }
         } else {
+#if SP200_PROFILE_KNOBS
+        if constexpr (INPLACE) {
+            // test hook (p.debug bit 64): every fifth tile stalls for ~20 us
+            // every 8th step, so its neighbours really have to wait for it
+            if ((p.debug & 64) && tid == 0 && tile % 5 == 2 && (s & 7) == 0) __nanosleep(20000);
+        }
+#endif
         if constexpr (INPLACE) {
             // polled by the last warp: it covers ghost rows above the stored
             // tile and has fewer stores per step than the interior warps, so
