@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
             // K3 destinations of this level-T plane
             [[maybe_unused]] double *nrow = nullptr, *yrow = nullptr, *zrow = nullptr;
             [[maybe_unused]] bool zb = false;
-            if constexpr (COMP) {
+            if constexpr (COMP && !INPLACE) {
                 if (u == T) {
                     nrow = ncol + (int64_t)pout * npz;
                     const int zo = pout - z0;
@@ -552,7 +552,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
                         }
                     }
                 } else if (store_plane && y_out[r]) {
-                    if constexpr (COMP) {
+                    if constexpr (COMP && !INPLACE) {
                         // band priority y, then z, then x (k_unstash_* skip
                         // in the same order); y and z bands are whole rows
                         double *row = nrow + (int64_t)r * nrs;
