@@ -74,7 +74,8 @@ struct TParams {
     // a plane wait until the tiles that read the cells they overwrite have
     // loaded that plane (per-tile progress counters, tiles taken in
     // dependency order through a ticket)
-    int *progress;            // [ntiles] input planes loaded (count), then [ntiles] = the ticket
+    int *progress;            // [nslots] input planes loaded (count) per unit, then [nslots] = the ticket
+    int nslots;
 };
 
 template <int T, int CY, int R, int S>
@@ -150,7 +151,7 @@ __device__ __forceinline__ void stg2_stream(double *p, double a, double b) {
 // fused in: CTAs whose tile touches a domain face, and every CTA at the two z
 // faces, copy the shell cells of their box from the stage into dst.
 template <int T, int CY, int R, int S, bool TMA, bool COMP, int CL, bool MIR = false, bool WP = false,
-          bool RING = false, bool XS1 = false, bool PS = false, bool INPLACE = false>
+          bool RING = false, bool XS1 = false, bool PS = false, bool INPLACE = false, bool ZCH = false>
 __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB)
     k_temporal(const TParams p, const __grid_constant__ CUtensorMap tmap) {
     using C = KCfg<T, CY, R, S>;
@@ -164,6 +165,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     // and, S - PD steps later, the producer, but not the whole CTA.
     static_assert(!PS || (TMA && !COMP && CL == 1 && !RING && !WP && S >= 5), "PS: plain TMA two-grid passes");
     static_assert(!INPLACE || COMP, "INPLACE: compressed passes only");
+    static_assert(!ZCH || INPLACE, "ZCH: z-chunked units of the in-place pass");
     constexpr int PD = WP ? S - 2 : (PS ? S - 3 : S - 1);  // stage prefetch distance
     constexpr int SPX = C::SPX, C0 = C::C0, PLANE = C::PLANE, PLANE_AL = C::PLANE_AL,
                   NT = C::NT;
@@ -208,7 +210,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
             if constexpr (INPLACE) {
                 // tiles are taken in dependency order: a CTA only ever waits
                 // for tiles with a lower ticket, which are running or done
-                reinterpret_cast<int *>(bar + C::NBAR)[0] = atomicAdd(p.progress + (int64_t)p.ntiles * PROG_STRIDE, 1);
+                reinterpret_cast<int *>(bar + C::NBAR)[0] = atomicAdd(p.progress + (int64_t)p.nslots * PROG_STRIDE, 1);
             }
             if constexpr (CL > 1) {
                 // arm phase 0 of every halo barrier: 64 doubles per row
@@ -254,8 +256,16 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
             // forward passes overwrite cells the lower neighbours read, so
             // tiles run in ascending order; backward passes in descending
             const int tk = reinterpret_cast<volatile int *>(bar + C::NBAR)[0];
-            tile = p.direction > 0 ? tk : p.ntiles - 1 - tk;
-            chunk = 0;
+            if constexpr (ZCH) {
+                // the tiles after the `split` full columns of the first
+                // launch, chunk-major: neighbours run the same chunk together
+                chunk = tk / p.tile_count2;
+                const int idx = p.split + tk % p.tile_count2;
+                tile = p.direction > 0 ? idx : p.ntiles - 1 - idx;
+            } else {
+                tile = p.direction > 0 ? tk : p.ntiles - 1 - tk;
+                chunk = 0;
+            }
         }
         z0 = p.zlo + chunk * uzc;
         z1 = min(z0 + uzc, p.zhi);
@@ -340,7 +350,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
         yb[r] = COMP && !INPLACE && (fwd ? (ty > 0 && yo < 2 * T) : (ty < p.tiles_y - 1 && yo >= OYc - 2 * T));
     }
     const int nchunks = (p.zhi - p.zlo + p.zc - 1) / p.zc;
-    const bool zband_chunk = COMP && !INPLACE && (fwd ? chunk > 0 : chunk < nchunks - 1);
+    const bool zband_chunk = COMP && (!INPLACE || ZCH) && (fwd ? chunk > 0 : chunk < nchunks - 1);
     // destinations, affine in the output plane pout and the row r:
     //   in place / x stash: ncol + pout * npz + r * nrs
     //   y stash: sy_col + (pout * hy2 + r) * srow;  z stash: sz_col + (kz * ny + r) * srow
@@ -359,7 +369,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     // INPLACE: the tiles that read the cells this tile's shifted stores overwrite
     // (forward: the lower x, y and diagonal neighbours), their cached
     // progress and the relaxed loads in flight
-    [[maybe_unused]] int rd_y = -1, rd_x = -1, rd_d = -1;
+    [[maybe_unused]] int rd_y = -1, rd_x = -1, rd_d = -1, my_slot = tile;
     [[maybe_unused]] int l_y = 0x7fffffff, l_x = 0x7fffffff, l_d = 0x7fffffff;
     [[maybe_unused]] int q_y[2] = {0, 0}, q_x[2] = {0, 0}, q_d[2] = {0, 0};  // polls in flight, by step parity
     if constexpr (INPLACE) {
@@ -368,9 +378,23 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
         if (hy) rd_y = tile + dd * p.tiles_x;
         if (hx) rd_x = tile + dd;
         if (hx && hy) rd_d = tile + dd * p.tiles_x + dd;
-        l_y = hy ? 0 : 0x7fffffff;
-        l_x = hx ? 0 : 0x7fffffff;
-        l_d = (hx && hy) ? 0 : 0x7fffffff;
+        // counter slots follow the ticket order (ascending tiles forward,
+        // descending backward).  ZCH: slots of this launch are (chunk,
+        // position after the full columns); the full columns finished with
+        // the first launch and need no wait
+        auto slot = [&](int t) {
+            if (t < 0) return -1;
+            const int idx = fwd ? t : p.ntiles - 1 - t;
+            if constexpr (ZCH) return idx < p.split ? -1 : chunk * p.tile_count2 + idx - p.split;
+            return idx;
+        };
+        my_slot = slot(tile);
+        rd_y = slot(rd_y);
+        rd_x = slot(rd_x);
+        rd_d = slot(rd_d);
+        l_y = rd_y >= 0 ? 0 : 0x7fffffff;
+        l_x = rd_x >= 0 ? 0 : 0x7fffffff;
+        l_d = rd_d >= 0 ? 0 : 0x7fffffff;
     }
     double *sy_col = COMP ? p.stash_y + ((int64_t)ky0 - (int64_t)p.zlo * p.hy2) * srow + rx0 + i0 + sxpad
                           : nullptr;
@@ -418,9 +442,13 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     // loop is unrolled by two) so the register rotation is pure renaming.
     // MODE 0: every cell interior (no select); 1: static x/y Dirichlet mask;
     // 2: mask plus per-level z-ring planes (domain z ends only).
-    auto levels = [&](int s, const double *cur, const double *prv, auto Qc, auto Mc) {
+    // ZB (ZCH only): this step's level-T plane is in the chunk's z band and
+    // goes to the z stash; a compile-time flag so that all other steps run the
+    // code of the whole-column instance
+    auto levels = [&](int s, const double *cur, const double *prv, auto Qc, auto Mc, auto Zc) {
         constexpr int Q = decltype(Qc)::value;
         constexpr int MODE = decltype(Mc)::value;
+        constexpr bool ZB = decltype(Zc)::value != 0;
 #pragma unroll
         for (int u = T; u >= 1; --u) {
             const int ui = (u > 1) ? u - 2 : 0;
@@ -451,6 +479,9 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
             // K3 destinations of this level-T plane
             [[maybe_unused]] double *nrow = nullptr, *yrow = nullptr, *zrow = nullptr;
             [[maybe_unused]] bool zb = false;
+            if constexpr (ZB) {
+                if (u == T) zrow = sz_col + (int64_t)(pout - z0 + kz_off) * zstride;
+            }
             if constexpr (COMP && !INPLACE) {
                 if (u == T) {
                     nrow = ncol + (int64_t)pout * npz;
@@ -572,7 +603,11 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
                         }
                     } else {
                         double *g = dcol + (int64_t)(pout + p.doff) * pz + (int64_t)r * p.ex;
-                        if (x_out[0] && x_out[1] && p.pair_store) {
+                        // ZB: the chunk's first (forward) / last (backward) 2T
+                        // planes land where the chunk below / above still
+                        // reads: they go to the z stash
+                        if constexpr (ZB) g = zrow + (int64_t)r * srow;
+                        if (x_out[0] && x_out[1] && (ZB || p.pair_store)) {
                             stg2_stream(g, v[r][0], v[r][1]);
                             if constexpr (MIR) stg2_stream(p.mir + (g - p.dst), v[r][0], v[r][1]);
                         } else {
@@ -684,9 +719,9 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
                             if (done == s + a && s + a < nload && mbar_test_wait(&bar[g % S], (g / S) & 1u)) done = s + a + 1;
                         }
                     }
-                    st_relaxed_s32(p.progress + tile * PROG_STRIDE, done);
+                    st_relaxed_s32(p.progress + my_slot * PROG_STRIDE, done);
                 } else if (s == nload) {
-                    st_relaxed_s32(p.progress + tile * PROG_STRIDE, 0x7ffffff0);
+                    st_relaxed_s32(p.progress + my_slot * PROG_STRIDE, 0x7ffffff0);
                 }
             }
         }
@@ -740,9 +775,19 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
         const int pmax = z0 - T + s - 1, pmin = z0 - T + s - 2 * T + 1;
         const bool zall = (pmin >= 0) && (pmax < p.nz);
         if (SP200_PROFILE_KNOBS && (p.debug & 1)) return;  // profiling builds only
-        if (wint && zall) levels(s, cur, prv, Qc, IC<0>{});
-        else if (zall) levels(s, cur, prv, Qc, IC<1>{});
-        else levels(s, cur, prv, Qc, IC<2>{});
+        bool zbs = false;
+        if constexpr (ZCH) zbs = zband_chunk && (unsigned)(s - 3 * T + 1 - zb_lo) < (unsigned)(2 * T);
+        if (ZCH && zbs) {
+            if constexpr (ZCH) {
+                if (wint && zall) levels(s, cur, prv, Qc, IC<0>{}, IC<1>{});
+                else if (zall) levels(s, cur, prv, Qc, IC<1>{}, IC<1>{});
+                else levels(s, cur, prv, Qc, IC<2>{}, IC<1>{});
+            }
+        } else {
+            if (wint && zall) levels(s, cur, prv, Qc, IC<0>{}, IC<0>{});
+            else if (zall) levels(s, cur, prv, Qc, IC<1>{}, IC<0>{});
+            else levels(s, cur, prv, Qc, IC<2>{}, IC<0>{});
+        }
         if constexpr (PS) {
             // this warp is done with the stage of step s
             __syncwarp();
@@ -1312,6 +1357,7 @@ struct UnstashArgs {
     int nx, ny, doff, zlo, zhi, zc, nchunks, ox, oy, tiles_x, tiles_y, T2, fwd, sxpad;
     const double *sx, *sy, *sz;
     int wx2, hy2;
+    int tile_lo, tile_hi;  // k_unstash_zt: the z-chunked tiles [tile_lo, tile_hi) of the in-place pass
 };
 
 __device__ __forceinline__ bool band_hit(int v, int tile, int ntiles, int o, int T2, int fwd) {
@@ -1364,6 +1410,22 @@ __global__ void k_unstash_z(UnstashArgs a) {
     const double *src = a.sz + (int64_t)blockIdx.x * ((a.nx + 2) & ~1) + a.sxpad;
     double *dst = a.data + ((int64_t)(z + a.doff) * a.ey + (y + a.doff)) * a.ex + a.doff;
     copy_row_batched(dst, src, a.nx);
+}
+
+// z stash of the in-place pass: only the tiles that ran as z-chunks stashed
+// their chunks' first / last 2T planes, whole stored rows of the tile (no x or
+// y band there); one CTA per stash row
+__global__ void k_unstash_zt(UnstashArgs a) {
+    const int y = blockIdx.x % a.ny, k = blockIdx.x / a.ny;
+    const int z = a.zlo + band_pos(k, a.zc, a.T2, a.fwd);
+    if (z >= a.zhi) return;
+    const int ty = y / a.oy;
+    const int t0 = max(ty * a.tiles_x, a.tile_lo), t1 = min((ty + 1) * a.tiles_x, a.tile_hi);
+    if (t0 >= t1) return;
+    const int xa = (t0 - ty * a.tiles_x) * a.ox, xb = min((t1 - ty * a.tiles_x) * a.ox, a.nx);
+    const double *src = a.sz + (int64_t)blockIdx.x * ((a.nx + 2) & ~1) + a.sxpad;
+    double *dst = a.data + ((int64_t)(z + a.doff) * a.ey + (y + a.doff)) * a.ex + a.doff;
+    copy_row_batched(dst + xa, src + xa, xb - xa);
 }
 
 // x stash: CTA = UX_ROWS rows y of one plane z (blockIdx.y); thread x =
@@ -1562,7 +1624,7 @@ static void comp_layout(int64_t nx, int64_t ny, int64_t depth, int64_t off, bool
 }
 
 template <int T, int CY, int R, int S, int CL = 1, bool MIRROR = false, bool WP = false,
-          bool XS1 = false, bool PS = false, bool INPLACE = false>
+          bool XS1 = false, bool PS = false>
 static int launch_cfg(const LaunchReq &q) {
     using C = KCfg<T, CY, R, S>;
     constexpr size_t SMEM_B = C::SMEM + (PS ? 8 * S : 0);  // + the PS empty barriers
@@ -1601,6 +1663,7 @@ static int launch_cfg(const LaunchReq &q) {
     p.zhi = (int)q.zhi;
     p.stash_x = p.stash_y = p.stash_z = nullptr;
     p.progress = nullptr;
+    p.nslots = 0;
     p.debug = (int)tuning().debug;
     p.wx2 = p.hy2 = 0;
 
@@ -1619,11 +1682,7 @@ static int launch_cfg(const LaunchReq &q) {
         kern = use_tma ? k_temporal<T, CY, R, S, true, false, CL>
                        : k_temporal<T, CY, R, S, false, false, CL>;
     } else if (comp) {
-        if constexpr (INPLACE)
-            kern = use_tma ? k_temporal<T, CY, R, S, true, true, 1, false, false, false, false, false, true>
-                           : k_temporal<T, CY, R, S, false, true, 1, false, false, false, false, false, true>;
-        else
-            kern = use_tma ? k_temporal<T, CY, R, S, true, true, 1> : k_temporal<T, CY, R, S, false, true, 1>;
+        kern = use_tma ? k_temporal<T, CY, R, S, true, true, 1> : k_temporal<T, CY, R, S, false, true, 1>;
     } else if constexpr (PS) {
         kern = use_tma ? k_temporal<T, CY, R, S, true, false, 1, false, false, false, false, true>
                        : k_temporal<T, CY, R, S, false, false, 1>;
@@ -1671,16 +1730,7 @@ static int launch_cfg(const LaunchReq &q) {
     CompLayout L;
     if (comp) {
         comp_layout<T, CY>(q.nx, q.ny, q.zhi - q.zlo, q.off, aligned, &L);
-        if constexpr (INPLACE) {
-            // whole columns, everything in place: no stash, one progress
-            // counter per tile and the ticket
-            L.zc = q.zhi - q.zlo;
-            L.nchunks = 1;
-            L.nx_stash = L.ny_stash = L.nz_stash = 0;
-            L.wx2 = L.hy2 = 0;
-        }
-        const int64_t inplace_bytes = INPLACE ? ((int64_t)p.ntiles + 1) * 4 * PROG_STRIDE : 0;
-        const int64_t need = 8 * (L.nx_stash + L.ny_stash + L.nz_stash) + inplace_bytes;
+        const int64_t need = 8 * (L.nx_stash + L.ny_stash + L.nz_stash);
         if (need > q.ws_bytes)
             return set_error(SP_EINVAL, "compressed pass needs %lld workspace bytes, got %lld",
                              (long long)need, (long long)q.ws_bytes);
@@ -1692,10 +1742,6 @@ static int launch_cfg(const LaunchReq &q) {
         p.stash_z = p.stash_y + L.ny_stash;
         p.wx2 = L.wx2;
         p.hy2 = L.hy2;
-        if constexpr (INPLACE) {
-            p.progress = reinterpret_cast<int *>(ws);
-            cudaMemsetAsync(ws, 0, (size_t)inplace_bytes, q.stream);
-        }
     } else {
         // z-chunking: choose the chunk count minimising (waves x steps per chunk)
         int64_t zc = tuning().zchunk;
@@ -1797,7 +1843,7 @@ static int launch_cfg(const LaunchReq &q) {
     launch_units<CL>(kern, grid, C::NT, SMEM_B, q.stream, p, tmap);
     count_launch();
     int rc = check_launch("k_temporal");
-    if (rc || !comp || INPLACE) return rc;
+    if (rc || !comp) return rc;
     UnstashArgs u;
     u.data = q.dst;
     u.ex = q.ex;
@@ -1840,6 +1886,156 @@ static int launch_cfg(const LaunchReq &q) {
 }
 
 
+
+
+// K3 in place (T levels, TMA-eligible arrays): geometry of the two launches.
+// `full` tiles (whole multiples of the SM count) march their whole column in
+// the first launch; the `rem` tiles after them run in the second launch as
+// z-chunks sized to fill the GPU once more, chunk-major.  Chunks of one tile
+// are decoupled by a z stash (the first / last 2T planes of a chunk, copied
+// into place by k_unstash_zt); x and y stay in place in both launches.
+struct InplaceLayout {
+    int ox, ex0, tiles_x, tiles_y, ntiles, full, rem;
+    int64_t zc2, nch2, lines, nz_stash;  // progress lines (128 B each), z-stash doubles
+};
+
+template <int T, int CY>
+static void inplace_layout(int64_t nx, int64_t ny, int64_t depth, int64_t off, InplaceLayout *L) {
+    tile_geometry<T, CY>(nx, ny, off, true, &L->ox, &L->ex0, &L->tiles_x, &L->tiles_y);
+    L->ntiles = L->tiles_x * L->tiles_y;
+    const int64_t slots = sm_count();
+    L->full = L->ntiles >= slots ? (int)((L->ntiles / slots) * slots) : 0;
+    L->rem = L->ntiles - L->full;
+    L->zc2 = depth;
+    L->nch2 = 1;
+    if (L->rem > 0 && !tuning().balanced_split) {
+        int64_t zc = tuning().zchunk2 > 0 ? std::min<int64_t>(tuning().zchunk2, depth)
+                                          : pick_zchunk(depth, L->rem, slots, T);
+        if (zc < 2 * T) zc = std::min<int64_t>(depth, 2 * T);
+        L->zc2 = zc;
+        L->nch2 = (depth + zc - 1) / zc;
+    }
+    if (L->nch2 == 1) {
+        // whole columns only: one launch
+        L->full = L->ntiles;
+        L->rem = 0;
+    }
+    L->lines = (L->full > 0 ? L->full + 1 : 0) + (L->rem > 0 ? (int64_t)L->rem * L->nch2 + 1 : 0);
+    L->nz_stash = L->rem > 0 ? (L->nch2 - 1) * 2 * T * ny * ((nx + 2) & ~1) : 0;
+}
+
+template <int T, int CY>
+static int64_t inplace_bytes(const InplaceLayout &L) {
+    return L.lines * 4 * PROG_STRIDE + 8 * L.nz_stash;
+}
+
+template <int T, int CY, int R, int S>
+static int launch_inplace(const LaunchReq &q) {
+    using C = KCfg<T, CY, R, S>;
+    InplaceLayout L;
+    inplace_layout<T, CY>(q.nx, q.ny, q.zhi - q.zlo, q.off, &L);
+    const int64_t need = inplace_bytes<T, CY>(L);
+    if (need > q.ws_bytes)
+        return set_error(SP_EINVAL, "compressed pass needs %lld workspace bytes, got %lld", (long long)need,
+                         (long long)q.ws_bytes);
+    TParams p;
+    memset(&p, 0, sizeof(p));
+    p.src = q.src;
+    p.dst = q.dst;
+    p.ex = q.ex;
+    p.ey = q.ey;
+    p.ez = q.ez;
+    p.nx = (int)q.nx;
+    p.ny = (int)q.ny;
+    p.nz = (int)q.nz;
+    p.off = (int)q.off;
+    p.doff = (int)q.doff;
+    p.direction = q.direction;
+    p.ox = L.ox;
+    p.ex0 = L.ex0;
+    p.tiles_x = L.tiles_x;
+    p.tiles_y = L.tiles_y;
+    p.ntiles = L.ntiles;
+    p.pair_store = ((q.off - q.doff) % 2 == 0) ? 1 : 0;
+    p.zlo = (int)q.zlo;
+    p.zhi = (int)q.zhi;
+    p.debug = (int)tuning().debug;
+    p.tile_count = L.ntiles;
+    p.split = 0x7fffffff;
+    CUtensorMap tmap;
+    memset(&tmap, 0, sizeof(tmap));
+    {
+        cuuint64_t dims[3] = {(cuuint64_t)q.ex, (cuuint64_t)q.ey, (cuuint64_t)q.ez};
+        cuuint64_t strides[2] = {(cuuint64_t)(q.ex * 8), (cuuint64_t)(q.ex * q.ey * 8)};
+        cuuint32_t box[3] = {(cuuint32_t)C::SPX, (cuuint32_t)C::PY, 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        CUresult r = encode_fn()(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)q.src, dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return set_error(SP_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    }
+    char *ws = reinterpret_cast<char *>(q.ws);
+    cudaMemsetAsync(ws, 0, (size_t)(L.lines * 4 * PROG_STRIDE), q.stream);
+    int *prog = reinterpret_cast<int *>(ws);
+    const int64_t depth = q.zhi - q.zlo;
+    if (L.full > 0) {
+        auto kern = k_temporal<T, CY, R, S, true, true, 1, false, false, false, false, false, true, false>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+        if (e != cudaSuccess) return set_error(SP_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+        TParams a = p;
+        a.zc = (int)depth;
+        a.progress = prog;
+        a.nslots = L.full;
+        kern<<<(unsigned)L.full, C::NT, C::SMEM, q.stream>>>(a, tmap);
+        count_launch();
+        int rc = check_launch("k_temporal (in place)");
+        if (rc) return rc;
+        prog += (int64_t)(L.full + 1) * PROG_STRIDE;
+    }
+    if (L.rem > 0) {
+        auto kern = k_temporal<T, CY, R, S, true, true, 1, false, false, false, false, false, true, true>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+        if (e != cudaSuccess) return set_error(SP_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+        TParams b = p;
+        b.zc = (int)L.zc2;
+        b.split = L.full;
+        b.tile_count2 = L.rem;
+        b.progress = prog;
+        b.nslots = (int)(L.rem * L.nch2);
+        b.stash_z = reinterpret_cast<double *>(ws + L.lines * 4 * PROG_STRIDE);
+        kern<<<(unsigned)(L.rem * L.nch2), C::NT, C::SMEM, q.stream>>>(b, tmap);
+        count_launch();
+        int rc = check_launch("k_temporal (in place, z chunks)");
+        if (rc) return rc;
+        UnstashArgs u;
+        memset(&u, 0, sizeof(u));
+        u.data = q.dst;
+        u.ex = q.ex;
+        u.ey = q.ey;
+        u.nx = (int)q.nx;
+        u.ny = (int)q.ny;
+        u.doff = (int)q.doff;
+        u.zlo = (int)q.zlo;
+        u.zhi = (int)q.zhi;
+        u.zc = (int)L.zc2;
+        u.nchunks = (int)L.nch2;
+        u.ox = L.ox;
+        u.oy = C::OY;
+        u.tiles_x = L.tiles_x;
+        u.tiles_y = L.tiles_y;
+        u.T2 = 2 * T;
+        u.fwd = q.direction > 0 ? 1 : 0;
+        u.sz = b.stash_z;
+        u.sxpad = L.ex0 & 1;
+        // the z-chunked tiles in tile order: the last `rem` (forward) or the first `rem` (backward)
+        u.tile_lo = q.direction > 0 ? L.full : 0;
+        u.tile_hi = q.direction > 0 ? L.ntiles : L.rem;
+        k_unstash_zt<<<(unsigned)((L.nch2 - 1) * 2 * T * q.ny), 128, 0, q.stream>>>(u);
+        count_launch();
+        return check_launch("k_unstash_zt");
+    }
+    return SP_OK;
+}
 
 #if SP200_AB
 
@@ -2185,7 +2381,7 @@ static int dispatch(int levels, const LaunchReq &q) {
         // T = 4 (the default depth): everything stored in place, ordered by
         // per-tile progress counters; tuning key 10 = 1 keeps the band stash
         if (levels == 4 && !tuning().k3_stash && uses_tma(q))
-            return launch_cfg<4, 32, 4, 4, 1, false, false, false, false, true>(q);
+            return launch_inplace<4, 32, 4, 4>(q);
         // K3: the CY = 32 instances, the geometry compressed_workspace sizes
         switch (levels) {
         case 1: return launch_cfg<1, 32, 4, 4>(q);
@@ -2295,11 +2491,14 @@ static int64_t comp_bytes_max(int64_t nx, int64_t ny, int64_t depth) {
         comp_layout<T, 32>(nx, ny, depth, (T - 1) + par, true, &L);
         best = std::max(best, L.nx_stash + L.ny_stash + L.nz_stash);
     }
-    // the in-place pass's progress counters and ticket
-    int ox, ex0, tx, ty;
-    tile_geometry<T, 32>(nx, ny, 0, false, &ox, &ex0, &tx, &ty);
-    const int64_t extra = ((int64_t)tx * ty + 1) * 4 * PROG_STRIDE + 64;
-    return 8 * best + 256 + extra;
+    // ... and over the in-place pass's counters and z stash
+    int64_t inp = 0;
+    for (int par = 0; par < 2; ++par) {
+        InplaceLayout L;
+        inplace_layout<T, 32>(nx, ny, depth, (T - 1) + par, &L);
+        inp = std::max(inp, inplace_bytes<T, 32>(L));
+    }
+    return std::max(8 * best, inp) + 256;
 }
 
 // The workspace of the launch sp_compressed picks for this array: the in-place
@@ -2308,12 +2507,13 @@ int64_t compressed_workspace_for(const double *data, int64_t ex, int64_t ey, int
                                  int64_t depth, int levels) {
     LaunchReq q{data, const_cast<double *>(data), ex, ey, 0, nx, ny, 0, 0, 0, 0, depth, 1, nullptr, 0, nullptr};
     if (levels == 4 && !tuning().k3_stash && data && uses_tma(q)) {
-        int ox, ex0, tx, ty, best = 0;
+        int64_t best = 0;
         for (int par = 0; par < 2; ++par) {
-            tile_geometry<4, 32>(nx, ny, 3 + par, true, &ox, &ex0, &tx, &ty);
-            best = std::max(best, tx * ty);
+            InplaceLayout L;
+            inplace_layout<4, 32>(nx, ny, depth, 3 + par, &L);
+            best = std::max(best, inplace_bytes<4, 32>(L));
         }
-        return ((int64_t)best + 1) * 4 * PROG_STRIDE + 256;
+        return best + 256;
     }
     return compressed_workspace(nx, ny, depth, levels);
 }

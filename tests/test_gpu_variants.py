@@ -67,16 +67,19 @@ def test_split_grid_pass(lib, two_launch, balanced):
     assert_bitwise(dst.interior_numpy(), exp)
 
 
-@pytest.mark.parametrize("stash", [0, 1])
+@pytest.mark.parametrize("mode", ["in_place", "whole_columns", "chunks_of_8", "stash"])
 @pytest.mark.parametrize("dims,pad", [((700, 500, 40), 4), ((90, 61, 30), 4), ((130, 130, 20), 5),
-                                       ((64, 9, 12), 4)])
-def test_compressed_in_place_and_stash(lib, stash, dims, pad):
-    """K3 at t=4: the default pass stores everything in place (per-tile
-    progress counters, tiles taken in dependency order, two rounds of tiles
-    on the 260-tile shape); tuning key 10 = 1 keeps the band stash and the
-    unstash kernels.  Forward and backward passes, bit-exact against the
-    oracle after every pass."""
-    assert lib.sp_set_tuning(10, stash) == 0
+                                       ((64, 9, 12), 4), ((300, 290, 70), 4)])
+def test_compressed_in_place_and_stash(lib, mode, dims, pad):
+    """K3 at t=4.  The default pass stores everything in place: per-tile
+    progress counters, tiles taken in dependency order; whole multiples of
+    the SM count march full columns, the remaining tiles follow in a second
+    launch as z-chunks decoupled by a z stash (260 tiles on the first shape).
+    Tuning key 7 = 1: whole columns only; key 8: chunk length; key 10 = 1:
+    the band stash and the unstash kernels.  Forward and backward passes,
+    bit-exact against the oracle after every pass."""
+    key, val = {"in_place": (7, 0), "whole_columns": (7, 1), "chunks_of_8": (8, 8), "stash": (10, 1)}[mode]
+    assert lib.sp_set_tuning(key, val) == 0
     try:
         d0 = oracle.make_storage(*dims, init="random", seed=5, lo=-1.0, hi=1.0)
         g = sp.create_grid(*dims, pad=pad, init="random", seed=5, lo=-1.0, hi=1.0)
@@ -87,7 +90,7 @@ def test_compressed_in_place_and_stash(lib, stash, dims, pad):
             exp = oracle.interior(oracle.sweeps(d0, dims, 4 * k), *dims)
             assert_bitwise(g.interior_numpy(), exp)
     finally:
-        lib.sp_set_tuning(10, 0)
+        lib.sp_set_tuning(key, 0)
 
 
 @pytest.mark.parametrize("layout", [6, 7, 8])
