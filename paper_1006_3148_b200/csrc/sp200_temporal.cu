@@ -2380,8 +2380,11 @@ static int dispatch(int levels, const LaunchReq &q) {
     if (q.direction != 0) {
         // T = 4 (the default depth): everything stored in place, ordered by
         // per-tile progress counters; tuning key 10 = 1 keeps the band stash
-        if (levels == 4 && !tuning().k3_stash && uses_tma(q))
-            return launch_inplace<4, 32, 4, 4>(q);
+        if (!tuning().k3_stash && uses_tma(q)) {
+            if (levels == 4) return launch_inplace<4, 32, 4, 4>(q);
+            if (levels == 3) return launch_inplace<3, 32, 4, 5>(q);
+            if (levels == 2) return launch_inplace<2, 32, 4, 6>(q);
+        }
         // K3: the CY = 32 instances, the geometry compressed_workspace sizes
         switch (levels) {
         case 1: return launch_cfg<1, 32, 4, 4>(q);
@@ -2506,12 +2509,15 @@ static int64_t comp_bytes_max(int64_t nx, int64_t ny, int64_t depth) {
 int64_t compressed_workspace_for(const double *data, int64_t ex, int64_t ey, int64_t nx, int64_t ny,
                                  int64_t depth, int levels) {
     LaunchReq q{data, const_cast<double *>(data), ex, ey, 0, nx, ny, 0, 0, 0, 0, depth, 1, nullptr, 0, nullptr};
-    if (levels == 4 && !tuning().k3_stash && data && uses_tma(q)) {
+    if (levels >= 2 && !tuning().k3_stash && data && uses_tma(q)) {
         int64_t best = 0;
         for (int par = 0; par < 2; ++par) {
             InplaceLayout L;
-            inplace_layout<4, 32>(nx, ny, depth, 3 + par, &L);
-            best = std::max(best, inplace_bytes<4, 32>(L));
+            switch (levels) {
+            case 2: inplace_layout<2, 32>(nx, ny, depth, 1 + par, &L); best = std::max(best, inplace_bytes<2, 32>(L)); break;
+            case 3: inplace_layout<3, 32>(nx, ny, depth, 2 + par, &L); best = std::max(best, inplace_bytes<3, 32>(L)); break;
+            default: inplace_layout<4, 32>(nx, ny, depth, 3 + par, &L); best = std::max(best, inplace_bytes<4, 32>(L)); break;
+            }
         }
         return best + 256;
     }

@@ -67,11 +67,12 @@ def test_split_grid_pass(lib, two_launch, balanced):
     assert_bitwise(dst.interior_numpy(), exp)
 
 
+@pytest.mark.parametrize("t", [2, 3, 4])
 @pytest.mark.parametrize("mode", ["in_place", "whole_columns", "chunks_of_8", "stash"])
 @pytest.mark.parametrize("dims,pad", [((700, 500, 40), 4), ((90, 61, 30), 4), ((130, 130, 20), 5),
                                        ((64, 9, 12), 4), ((300, 290, 70), 4)])
-def test_compressed_in_place_and_stash(lib, mode, dims, pad):
-    """K3 at t=4.  The default pass stores everything in place: per-tile
+def test_compressed_in_place_and_stash(lib, mode, dims, pad, t):
+    """K3 at t=2..4.  The default pass stores everything in place: per-tile
     progress counters, tiles taken in dependency order; whole multiples of
     the SM count march full columns, the remaining tiles follow in a second
     launch as z-chunks decoupled by a z stash (260 tiles on the first shape).
@@ -83,11 +84,11 @@ def test_compressed_in_place_and_stash(lib, mode, dims, pad):
     try:
         d0 = oracle.make_storage(*dims, init="random", seed=5, lo=-1.0, hi=1.0)
         g = sp.create_grid(*dims, pad=pad, init="random", seed=5, lo=-1.0, hi=1.0)
-        cfg = sp.PipelineConfig(spec=sp.BlockSpec(dims[0], 8, 8), t=4, grid_mode="compressed")
+        cfg = sp.PipelineConfig(spec=sp.BlockSpec(dims[0], 8, 8), t=t, grid_mode="compressed")
         eng = sp.PipelineEngine(cfg, g)
         for k in range(1, 4):
             eng.run_pass(1 if k % 2 == 1 else -1)
-            exp = oracle.interior(oracle.sweeps(d0, dims, 4 * k), *dims)
+            exp = oracle.interior(oracle.sweeps(d0, dims, t * k), *dims)
             assert_bitwise(g.interior_numpy(), exp)
     finally:
         lib.sp_set_tuning(key, 0)

@@ -1,4 +1,4 @@
-"""Stress the in-place K3 pass (T=4): the same passes with the band-stash path
+"""Stress the in-place K3 pass (--t 2..4): the same passes with the band-stash path
 (tuning key 10 = 1) must leave bit-identical storage, pass after pass, on
 shapes with one and several rounds of tiles, with and without another stream
 keeping some SMs busy (so tiles of one pass start at different times and the
@@ -19,6 +19,7 @@ import paper_1006_3148_b200 as sp
 ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--passes", type=int, default=4)
+ap.add_argument("--t", type=int, default=4)
 a = ap.parse_args()
 L = sp._lib.load()
 
@@ -28,7 +29,7 @@ bad = 0
 total = 0
 side = torch.cuda.Stream()
 for dims in SHAPES:
-    cfg = sp.PipelineConfig(spec=sp.BlockSpec(dims[0], 8, 8), t=4, grid_mode="compressed")
+    cfg = sp.PipelineConfig(spec=sp.BlockSpec(dims[0], 8, 8), t=a.t, grid_mode="compressed")
     for rep in range(a.reps):
         for disturb in (False, True):
             res = []
