@@ -145,13 +145,14 @@ int sp_temporal(const double *src, double *dst, int64_t ex, int64_t ey, int64_t 
  * Ring cells are read at the source frame (the caller writes the faces there
  * first); the faces are written at the destination frame afterwards when
  * faces != NULL.  A tile's shifted stores land in the read regions of its
- * lower (forward) or upper (backward) neighbours.  At levels = 4 on a
- * TMA-eligible array every output is stored in place: tiles are taken in
- * dependency order and a tile's stores of a plane wait until those neighbours
- * have loaded it (per-tile progress counters in `workspace`, 128 bytes per
- * tile).  Otherwise the outputs that would land in another tile's read
- * region go through `workspace` (a band stash) and are copied into place by
- * a second kernel.
+ * lower (forward) or upper (backward) neighbours.  At levels 2..4 on a
+ * TMA-eligible array they are stored in place: tiles are taken in dependency
+ * order and a tile's stores of a plane wait until those neighbours have
+ * loaded it (progress counters in `workspace`, 128 bytes per unit; tiles
+ * beyond whole multiples of the SM count run as z-chunks whose first / last
+ * 2*levels planes go through a z stash in `workspace`).  Otherwise the
+ * outputs that would land in another tile's read region go through
+ * `workspace` (a band stash) and are copied into place by a second kernel.
  * sp_compressed_workspace() returns the workspace bytes for a pass over
  * `depth` = zhi - zlo planes, the worst case over every path and tile layout
  * a launch may pick; sp_compressed_workspace_for() returns the bytes for the
@@ -235,8 +236,10 @@ int sp_unpack_boxes(double *grid, int64_t ex, int64_t ey, int64_t ez, int nbox,
  * key 8: z-chunk length of the remaining tiles in a split K2 pass (0 = model)
  * key 9: K2 kernel layout (A/B builds only; 0 = the product's lane-pair
  *        k_temporal, 6-10 = k_tm with the pipeline state in tensor memory)
- * key 10: 1 = sp_compressed at levels 4 keeps the band stash and the unstash
- *        kernels instead of storing in place */
+ * key 10: 1 = sp_compressed keeps the band stash and the unstash kernels at
+ *        every depth instead of storing in place
+ * (keys 7 and 8 also steer the in-place pass: 7 = 1 whole columns only,
+ *  8 = z-chunk length of its second launch) */
 int sp_set_tuning(int key, int64_t value);
 
 /* Query: 1 if the TMA loader applies to a grid with row extent `ex`. */

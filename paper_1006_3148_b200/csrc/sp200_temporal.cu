@@ -318,7 +318,8 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
         y_out[r] = (jr >= T - 1) && (jr < T - 1 + OYc) && (y < p.ny);
     }
     // warps without ring cells skip the select
-    const bool wint = !__any_sync(0xffffffffu, ringb != 0u);
+    // (profiling builds, p.debug bit 128: treat every warp as interior to time the ring selects; wrong results)
+    const bool wint = !__any_sync(0xffffffffu, ringb != 0u) || (SP200_PROFILE_KNOBS && (p.debug & 128));
     [[maybe_unused]] const bool ring_tile =
         RING && (x0 == 0 || y0 == 0 || x0 + p.ox >= p.nx || y0 + OYc >= p.ny);
 
