@@ -180,10 +180,11 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     uint64_t *bar = reinterpret_cast<uint64_t *>(lev + C::NLEV * PLANE_AL);
 
     const int tid = threadIdx.x;
-    // K3: the warp index through a shuffle is provably warp-uniform, so the
-    // band predicates and stash row addresses go to the uniform datapath
-    // (measured +7 % for K3; the same change costs K2 2 %)
-    const int lane = tid & 31, warp = COMP ? __shfl_sync(0xffffffffu, tid >> 5, 0) : tid >> 5;
+    // The warp index through a shuffle is provably warp-uniform, so the row
+    // predicates and per-warp addresses go to the uniform datapath.  Measured
+    // per instance: K3 +7 % (stash) / +6 % (in place); K2 at 512^3 T=4 +1.0 %,
+    // T=3 +2.7 %, T=2 -3.2 % (profiles/r02_s4_ab_uwarp.log), so T >= 3 only
+    const int lane = tid & 31, warp = (COMP || T >= 3) ? __shfl_sync(0xffffffffu, tid >> 5, 0) : tid >> 5;
     const int i0 = 2 * lane;   // region column of this lane's first cell
     const int j0 = warp * R;   // first region row
 
