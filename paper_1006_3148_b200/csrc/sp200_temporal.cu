@@ -131,6 +131,17 @@ __device__ __forceinline__ void stg2_stream(double *p, double a, double b) {
 // tile-fastest schedule (the reference needs the same order-dependence only
 // because its blocks run in lexicographic order, sp/grid.py:195-204).
 //
+// INPLACE (COMP, T >= 2, TMA): no x / y stash.  Every output is stored in
+// place; the tiles run in dependency order (a ticket per CTA: ascending tiles
+// forward, descending backward) and a tile's stores of a plane wait until the
+// three neighbours whose read regions they land in have loaded that plane
+// (per-unit progress counters in global memory, one 128-byte line each;
+// thread 0 publishes after the step barrier, lane 0 of the last warp polls
+// before it).  This is the paper's relaxed synchronisation (Eq. 3) between
+// SMs.  ZCH: the units of the second launch, z-chunks of the tiles beyond
+// whole multiples of the SM count, chunk-major; chunks are decoupled by a z
+// stash (the chunk's first / last 2T planes, k_unstash_zt).
+//
 // CL > 1 (two-grid only): a thread-block cluster of CL CTAs stacked in y
 // shares one overlapped tile of 64 x CL*CY region rows, so the ghost zone is
 // paid once per cluster instead of once per CTA.  Each step the boundary
