@@ -123,6 +123,11 @@ __device__ __forceinline__ void cp_async_8(void *smem_dst, const void *gsrc, uin
                  "l"(gsrc), "r"(src_bytes)
                  : "memory");
 }
+// 16-byte copy through L2 only (no L1 allocation: the source may be a line
+// other SMs keep writing)
+__device__ __forceinline__ void cp_async_16_cg(void *smem_dst, const void *gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() {
     asm volatile("cp.async.commit_group;" ::: "memory");
 }

@@ -46,6 +46,10 @@ namespace sp200 {
 // K3 in place: one progress counter per 128-byte line
 constexpr int PROG_STRIDE = 32;
 
+#ifndef SP200_X
+#define SP200_X 0
+#endif
+
 struct TParams {
     const double *src;
     double *dst;
@@ -77,6 +81,23 @@ struct TParams {
     int *progress;            // [nslots] input planes loaded (count) per unit, then [nslots] = the ticket
     int nslots;
 };
+
+// K3 in place: wait until the neighbours' progress counters reach `need`.
+// Out of line on purpose: the loop is practically never entered, but inlined
+// into the step function it cost the whole kernel 7 % (C3 581 vs 621 GLUP/s
+// with the loop compiled out).
+__device__ __noinline__ void inplace_wait(const int *progress, int rd0, int rd1, int rd2, int need) {
+    int spins = 0;
+    for (;;) {
+        int c = 0x7fffffff;
+        if (rd0 >= 0) c = min(c, ld_acquire_s32(progress + rd0 * PROG_STRIDE));
+        if (rd1 >= 0) c = min(c, ld_acquire_s32(progress + rd1 * PROG_STRIDE));
+        if (rd2 >= 0) c = min(c, ld_acquire_s32(progress + rd2 * PROG_STRIDE));
+        if (c >= need) return;
+        if (++spins > (1 << 26)) __trap();  // a broken dependency order, never a slow neighbour
+        __nanosleep(32);
+    }
+}
 
 template <int T, int CY, int R, int S>
 struct KCfg {
@@ -382,10 +403,20 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
     // INPLACE: the tiles that read the cells this tile's shifted stores overwrite
     // (forward: the lower x, y and diagonal neighbours), their cached
     // progress and the relaxed loads in flight
-    [[maybe_unused]] int rd_y = -1, rd_x = -1, rd_d = -1, my_slot = tile;
-    [[maybe_unused]] int l_y = 0x7fffffff, l_x = 0x7fffffff, l_d = 0x7fffffff;
-    [[maybe_unused]] int q_y[2] = {0, 0}, q_x[2] = {0, 0}, q_d[2] = {0, 0};  // polls in flight, by step parity
+    // The bookkeeping state lives in shared memory (bk[]: the ticket, this
+    // unit's counter slot, the neighbours' slots rd, their last seen counts l,
+    // the polls in flight q by step parity), touched by two threads only: in
+    // registers it cost every thread a dozen of its 254 and the main loop
+    // rematerialised addresses instead
+    [[maybe_unused]] volatile int *bk = reinterpret_cast<volatile int *>(bar + C::NBAR);
+    enum { BK_TICKET = 0, BK_SLOT = 1, BK_RD = 2, BK_L = 5 };  // rd[3], l[3]
+    // polls in flight: q[parity][neighbour], 16 bytes each (cp.async.cg
+    // copies the head of the neighbour's counter line here, no register held
+    // while the load is in flight)
+    [[maybe_unused]] volatile int *bq = reinterpret_cast<volatile int *>(
+        (reinterpret_cast<uintptr_t>(bk + 8) + 15) & ~(uintptr_t)15);
     if constexpr (INPLACE) {
+        int rd_y = -1, rd_x = -1, rd_d = -1;
         const int dd = fwd ? -1 : 1;
         const bool hy = fwd ? ty > 0 : ty < p.tiles_y - 1, hx = fwd ? tx > 0 : tx < p.tiles_x - 1;
         if (hy) rd_y = tile + dd * p.tiles_x;
@@ -401,13 +432,16 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
             if constexpr (ZCH) return idx < p.split ? -1 : chunk * p.tile_count2 + idx - p.split;
             return idx;
         };
-        my_slot = slot(tile);
-        rd_y = slot(rd_y);
-        rd_x = slot(rd_x);
-        rd_d = slot(rd_d);
-        l_y = rd_y >= 0 ? 0 : 0x7fffffff;
-        l_x = rd_x >= 0 ? 0 : 0x7fffffff;
-        l_d = rd_d >= 0 ? 0 : 0x7fffffff;
+        if (tid == NT - 32) {
+            const int rd[3] = {slot(rd_y), slot(rd_x), slot(rd_d)};
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                bk[BK_RD + k] = rd[k];
+                bk[BK_L + k] = rd[k] >= 0 ? 0 : 0x7fffffff;
+                bq[4 * k] = bq[4 * (3 + k)] = 0;
+            }
+        }
+        if (tid == 0) bk[BK_SLOT] = slot(tile);
     }
     double *sy_col = COMP ? p.stash_y + ((int64_t)ky0 - (int64_t)p.zlo * p.hy2) * srow + rx0 + i0 + sxpad
                           : nullptr;
@@ -673,7 +707,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
             // tile and has fewer stores per step than the interior warps, so
             // the few dozen instructions here do not make it the last one at
             // the barrier
-            if (tid == NT - 32) {
+            if (tid == NT - 32 && !(SP200_X & 1)) {
                 // this step's level-T stores (plane index s - 2T + 1 of the
                 // column) land on input plane s - 2T + 1 -/+ T of the source
                 // frame: the neighbours must have loaded it.  l_* were loaded
@@ -682,30 +716,25 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
                 // polls issued two steps ago (a counter line that another SM
                 // keeps writing takes longer than one step to read)
                 constexpr int QQ = decltype(Qc)::value;
-                l_y = max(l_y, q_y[QQ]);
-                l_x = max(l_x, q_x[QQ]);
-                l_d = max(l_d, q_d[QQ]);
-                if (min(l_y, min(l_x, l_d)) < need) {
-                    int spins = 0;
-                    for (;;) {
-                        int c = 0x7fffffff;
-                        if (rd_y >= 0) c = min(c, ld_acquire_s32(p.progress + rd_y * PROG_STRIDE));
-                        if (rd_x >= 0) c = min(c, ld_acquire_s32(p.progress + rd_x * PROG_STRIDE));
-                        if (rd_d >= 0) c = min(c, ld_acquire_s32(p.progress + rd_d * PROG_STRIDE));
-                        if (c >= need) break;
-                        if (++spins > (1 << 26)) __trap();  // a broken dependency order, never a slow neighbour
-                        __nanosleep(32);
-                    }
+                cp_async_wait<1>();  // the polls of two steps ago have landed
+                int rd[3], l[3];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    rd[k] = bk[BK_RD + k];
+                    l[k] = max(bk[BK_L + k], bq[4 * (3 * QQ + k)]);
                 }
+                if (min(l[0], min(l[1], l[2])) < need) inplace_wait(p.progress, rd[0], rd[1], rd[2], need);
                 // re-poll a neighbour only when its last seen count runs out
                 // within three steps (forward passes have 3T-1 planes of
                 // slack, so this is one poll every ~10 steps; backward T-1)
-                {
-                    const int soon = need + 3;
-                    if (rd_y >= 0 && l_y < soon) q_y[QQ] = ld_relaxed_s32(p.progress + rd_y * PROG_STRIDE);
-                    if (rd_x >= 0 && l_x < soon) q_x[QQ] = ld_relaxed_s32(p.progress + rd_x * PROG_STRIDE);
-                    if (rd_d >= 0 && l_d < soon) q_d[QQ] = ld_relaxed_s32(p.progress + rd_d * PROG_STRIDE);
+                const int soon = need + 3;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    bk[BK_L + k] = l[k];
+                    if (rd[k] >= 0 && l[k] < soon)
+                        cp_async_16_cg(const_cast<int *>(bq) + 4 * (3 * QQ + k), p.progress + rd[k] * PROG_STRIDE);
                 }
+                cp_async_commit();
             }
         }
         if (!(SP200_PROFILE_KNOBS && (p.debug & 4))) __syncthreads();
@@ -720,7 +749,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
             // published by thread 0 after the barrier (warp 0 covers ghost
             // rows too); every counter has its own 128-byte line: counters
             // sharing a sector ran 3x slower
-            if (tid == 0) {
+            if (tid == 0 && !(SP200_X & 2)) {
                 // input planes this tile has in shared memory: step s's, plus
                 // the prefetched stages that have already landed
                 if (s < nload) {
@@ -732,9 +761,9 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
                             if (done == s + a && s + a < nload && mbar_test_wait(&bar[g % S], (g / S) & 1u)) done = s + a + 1;
                         }
                     }
-                    st_relaxed_s32(p.progress + my_slot * PROG_STRIDE, done);
+                    st_relaxed_s32(p.progress + bk[BK_SLOT] * PROG_STRIDE, done);
                 } else if (s == nload) {
-                    st_relaxed_s32(p.progress + my_slot * PROG_STRIDE, 0x7ffffff0);
+                    st_relaxed_s32(p.progress + bk[BK_SLOT] * PROG_STRIDE, 0x7ffffff0);
                 }
             }
         }
@@ -1987,19 +2016,45 @@ static int launch_inplace(const LaunchReq &q) {
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return set_error(SP_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     }
+#if SP200_PROFILE_KNOBS
+    // timing experiment (p.debug bit 1024, wrong results): store out of place
+    // into a scratch array, to separate the in-place memory pattern from the
+    // kernel's instruction stream
+    if (tuning().debug & 1024) {
+        static double *scratch = nullptr;
+        static size_t scratch_n = 0;
+        const size_t n = (size_t)(q.ex * q.ey * q.ez);
+        if (scratch_n < n) {
+            if (scratch) cudaFree(scratch);
+            cudaMalloc(&scratch, n * sizeof(double));
+            scratch_n = n;
+        }
+        p.dst = scratch;
+    }
+#endif
     char *ws = reinterpret_cast<char *>(q.ws);
     cudaMemsetAsync(ws, 0, (size_t)(L.lines * 4 * PROG_STRIDE), q.stream);
     int *prog = reinterpret_cast<int *>(ws);
     const int64_t depth = q.zhi - q.zlo;
     if (L.full > 0) {
         auto kern = k_temporal<T, CY, R, S, true, true, 1, false, false, false, false, false, true, false>;
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM + 192);
         if (e != cudaSuccess) return set_error(SP_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
         TParams a = p;
         a.zc = (int)depth;
         a.progress = prog;
         a.nslots = L.full;
-        kern<<<(unsigned)L.full, C::NT, C::SMEM, q.stream>>>(a, tmap);
+#if SP200_PROFILE_KNOBS
+        // timing experiment (p.debug bit 2048, wrong results): the two-grid
+        // instance on the same units, no tickets and no waits
+        if (tuning().debug & 2048) {
+            auto k2 = k_temporal<T, CY, R, S, true, false, 1>;
+            cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM + 192);
+            a.tile_count = L.full;
+            k2<<<(unsigned)L.full, C::NT, C::SMEM + 192, q.stream>>>(a, tmap);
+        } else
+#endif
+        kern<<<(unsigned)L.full, C::NT, C::SMEM + 192, q.stream>>>(a, tmap);
         count_launch();
         int rc = check_launch("k_temporal (in place)");
         if (rc) return rc;
@@ -2007,7 +2062,7 @@ static int launch_inplace(const LaunchReq &q) {
     }
     if (L.rem > 0) {
         auto kern = k_temporal<T, CY, R, S, true, true, 1, false, false, false, false, false, true, true>;
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM + 192);
         if (e != cudaSuccess) return set_error(SP_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
         TParams b = p;
         b.zc = (int)L.zc2;
@@ -2016,7 +2071,7 @@ static int launch_inplace(const LaunchReq &q) {
         b.progress = prog;
         b.nslots = (int)(L.rem * L.nch2);
         b.stash_z = reinterpret_cast<double *>(ws + L.lines * 4 * PROG_STRIDE);
-        kern<<<(unsigned)(L.rem * L.nch2), C::NT, C::SMEM, q.stream>>>(b, tmap);
+        kern<<<(unsigned)(L.rem * L.nch2), C::NT, C::SMEM + 192, q.stream>>>(b, tmap);
         count_launch();
         int rc = check_launch("k_temporal (in place, z chunks)");
         if (rc) return rc;
