@@ -762,7 +762,10 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
                     int done = s + 1;
                     if constexpr (TMA) {
 #pragma unroll
-                        for (int a = 1; a < PD; ++a) {
+                        // (prefetched stages count only at T = 2, whose backward
+                        // passes have one plane of slack: at T >= 3 the probes cost
+                        // more than the slack buys, 606 vs 570 GLUP/s at T=3)
+                        for (int a = 1; a < (T <= 2 ? PD : 1); ++a) {
                             const uint32_t g = gbase + (uint32_t)(s + a);
                             if (done == s + a && s + a < nload && mbar_test_wait(&bar[g % S], (g / S) & 1u)) done = s + a + 1;
                         }
