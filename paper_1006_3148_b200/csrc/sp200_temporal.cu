@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
             for (int k = 0; k < 3; ++k) {
                 bk[BK_RD + k] = rd[k];
                 bk[BK_L + k] = rd[k] >= 0 ? 0 : 0x7fffffff;
-                bq[4 * k] = bq[4 * (3 + k)] = 0;
+                bq[4 * k] = bq[4 * (3 + k)] = rd[k] >= 0 ? 0 : 0x7fffffff;
             }
         }
         if (tid == 0) bk[BK_SLOT] = slot(tile);
@@ -723,22 +723,31 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
                 // keeps writing takes longer than one step to read)
                 constexpr int QQ = decltype(Qc)::value;
                 cp_async_wait<1>();  // the polls of two steps ago have landed
-                int rd[3], l[3];
+                const int rd0 = bk[BK_RD], rd1 = bk[BK_RD + 1], rd2 = bk[BK_RD + 2];
+                if constexpr (T >= 3) {
+                    // every present neighbour is polled every step (the slots
+                    // of absent ones hold 0x7fffffff and are never polled)
+                    if (min(bq[4 * (3 * QQ)], min(bq[4 * (3 * QQ + 1)], bq[4 * (3 * QQ + 2)])) < need)
+                        inplace_wait(p.progress, rd0, rd1, rd2, need);
+                    if (rd0 >= 0) cp_async_16_cg(const_cast<int *>(bq) + 4 * (3 * QQ), p.progress + rd0 * PROG_STRIDE);
+                    if (rd1 >= 0) cp_async_16_cg(const_cast<int *>(bq) + 4 * (3 * QQ + 1), p.progress + rd1 * PROG_STRIDE);
+                    if (rd2 >= 0) cp_async_16_cg(const_cast<int *>(bq) + 4 * (3 * QQ + 2), p.progress + rd2 * PROG_STRIDE);
+                } else {
+                    // T = 2 (short steps): keep the last seen counts and
+                    // re-poll a neighbour only when its count runs out within
+                    // three steps (487 vs 464 GLUP/s at 600^3)
+                    const int rd[3] = {rd0, rd1, rd2};
+                    int l[3];
 #pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    rd[k] = bk[BK_RD + k];
-                    l[k] = max(bk[BK_L + k], bq[4 * (3 * QQ + k)]);
-                }
-                if (min(l[0], min(l[1], l[2])) < need) inplace_wait(p.progress, rd[0], rd[1], rd[2], need);
-                // re-poll a neighbour only when its last seen count runs out
-                // within three steps (forward passes have 3T-1 planes of
-                // slack, so this is one poll every ~10 steps; backward T-1)
-                const int soon = need + 3;
+                    for (int k = 0; k < 3; ++k) l[k] = max(bk[BK_L + k], bq[4 * (3 * QQ + k)]);
+                    if (min(l[0], min(l[1], l[2])) < need) inplace_wait(p.progress, rd0, rd1, rd2, need);
+                    const int soon = need + 3;
 #pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    bk[BK_L + k] = l[k];
-                    if (rd[k] >= 0 && l[k] < soon)
-                        cp_async_16_cg(const_cast<int *>(bq) + 4 * (3 * QQ + k), p.progress + rd[k] * PROG_STRIDE);
+                    for (int k = 0; k < 3; ++k) {
+                        bk[BK_L + k] = l[k];
+                        if (rd[k] >= 0 && l[k] < soon)
+                            cp_async_16_cg(const_cast<int *>(bq) + 4 * (3 * QQ + k), p.progress + rd[k] * PROG_STRIDE);
+                    }
                 }
                 cp_async_commit();
             }
