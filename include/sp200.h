@@ -156,7 +156,8 @@ int sp_temporal(const double *src, double *dst, int64_t ex, int64_t ey, int64_t 
  * sp_compressed_workspace() returns the workspace bytes for a pass over
  * `depth` = zhi - zlo planes, the worst case over every path and tile layout
  * a launch may pick; sp_compressed_workspace_for() returns the bytes for the
- * path sp_compressed takes on this array (the in-place pass needs no stash).
+ * path sp_compressed takes on this array (the in-place pass needs no x / y
+ * band stash, only its counters and the small z stash).
  * sp_compressed returns SP_EINVAL when `workspace_bytes` is smaller than the
  * launch needs.
  */
