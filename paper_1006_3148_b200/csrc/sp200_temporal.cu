@@ -46,10 +46,6 @@ namespace sp200 {
 // K3 in place: one progress counter per 128-byte line
 constexpr int PROG_STRIDE = 32;
 
-#ifndef SP200_X
-#define SP200_X 0
-#endif
-
 struct TParams {
     const double *src;
     double *dst;
@@ -713,7 +709,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
             // tile and has fewer stores per step than the interior warps, so
             // the few dozen instructions here do not make it the last one at
             // the barrier
-            if (tid == NT - 32 && !(SP200_X & 1)) {
+            if (tid == NT - 32) {
                 // this step's level-T stores (plane index s - 2T + 1 of the
                 // column) land on input plane s - 2T + 1 -/+ T of the source
                 // frame: the neighbours must have loaded it.  l_* were loaded
@@ -764,7 +760,7 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
             // published by thread 0 after the barrier (warp 0 covers ghost
             // rows too); every counter has its own 128-byte line: counters
             // sharing a sector ran 3x slower
-            if (tid == 0 && !(SP200_X & 2)) {
+            if (tid == 0) {
                 // input planes this tile has in shared memory: step s's, plus
                 // the prefetched stages that have already landed
                 if (s < nload) {
