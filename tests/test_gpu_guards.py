@@ -111,3 +111,39 @@ def test_compressed_workspace_covers_every_layout():
     a = oracle.make_storage(n, n, n, init="random", seed=9, lo=-1.0, hi=1.0)
     exp = oracle.interior(oracle.sweeps(a, (n, n, n), 2), n, n, n)
     assert_bitwise(g.interior_numpy(), exp)
+
+
+@pytest.mark.parametrize("t", [2, 3, 4])
+def test_in_place_workspace_is_small_and_guarded(t):
+    """The in-place K3 pass (t = 2..4) needs its progress counters and the z
+    stash of the z-chunked tiles only: sp_compressed_workspace_for returns
+    that size for the array (far below the band stash), a launch inside
+    canaries with exactly that many bytes touches nothing outside and is
+    bit-exact, and a smaller workspace fails with ValueError."""
+    n = (300, 290, 70)
+    L = sp._lib.load()
+    bg, g = guarded_grid(*n, pad=4, init="random", seed=9, lo=-1.0, hi=1.0)
+    ex, ey, _ = g.extents
+    from paper_1006_3148_b200.kernel import _ptr
+    small = int(L.sp_compressed_workspace_for(_ptr(g.data), ex, ey, n[0], n[1], n[2], t))
+    worst = int(L.sp_compressed_workspace(n[0], n[1], n[2], t))
+    assert 0 < small <= worst
+    L.sp_set_tuning(7, 1)   # whole columns only: counters, no z stash
+    try:
+        tiny = int(L.sp_compressed_workspace_for(_ptr(g.data), ex, ey, n[0], n[1], n[2], t))
+    finally:
+        L.sp_set_tuning(7, 0)
+    assert tiny < 64 * 1024 and tiny < worst // 50
+    words = small // 8 + 1
+    wbuf = torch.full((words + 2 * GUARD,), CANARY, dtype=torch.float64, device="cuda")
+    ws = wbuf[GUARD:GUARD + words].view(torch.uint8)[:small]
+    with pytest.raises(ValueError):
+        compressed_pass(g, t, 1, g.alignment, ws[:128])
+    for direction in (1, -1):
+        compressed_pass(g, t, direction, g.alignment, ws)
+        g.alignment += t * direction
+    assert intact(bg, g.data.numel())
+    assert bool(torch.all(wbuf[:GUARD] == CANARY)) and bool(torch.all(wbuf[GUARD + words:] == CANARY))
+    a = oracle.make_storage(*n, init="random", seed=9, lo=-1.0, hi=1.0)
+    exp = oracle.interior(oracle.sweeps(a, n, 2 * t), *n)
+    assert_bitwise(g.interior_numpy(), exp)
