@@ -749,6 +749,10 @@ __global__ void __launch_bounds__(KCfg<T, CY, R, S>::NT, KCfg<T, CY, R, S>::MINB
             }
         }
         if (!(SP200_PROFILE_KNOBS && (p.debug & 4))) __syncthreads();
+        // the stage was written by the async proxy and only one thread watched
+        // its mbarrier: order every thread's generic reads after those writes
+        // (measured free: 810 vs 808 GLUP/s)
+        if constexpr (TMA) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         if constexpr (TMA) {
             if (tid == 0 && s + PD < nload && !(SP200_PROFILE_KNOBS && (p.debug & 2))) issue(s + PD);
         } else {
